@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""Benchmark: text GB/s scanned per pattern (device-timed), % of B200 HBM peak.
+
+One STEP = one pass of the whole hot path over the config's synthetic text:
+  A1  device histogram of the (owned) text  [+ NCCL all_reduce for N > 1]
+  A2  rarest-first order pi per pattern (host, from the histogram)
+  A3-A7 one counting search launch per pattern (TMA staging, peeled packed-byte
+      compares, early exit, popcount/atomics)          [+ all_reduce of counts]
+Default workload = BASELINE.json configs[1] (c2, English-like 256 MiB text, 100
+patterns at each m in {2,4,...,1024}).  value = text bytes x patterns / step time
+(GB = 1e9 B), whole job.  Reporting (A8) is timed in the same run as the
+`report` sub-object.  Multi-GPU: weak scaling, each rank holds a 256 MiB shard
+of an N x 256 MiB text (+1023-byte halo) and counts its owned alignments.
+
+`--impl reference` times the CPU oracle (oracle/, plain Alg. 1) on the host
+cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0
+METRIC = "text GB/s scanned per pattern (device-timed) vs m; % of B200 HBM peak, 1/2/4/8 GPU"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["native", "reference"], default="native")
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--per-m", type=int, default=None, help="patterns per length (default: config's)")
+    ap.add_argument("--lengths", default=None, help="comma list of pattern lengths (default: config's)")
+    ap.add_argument("--shard-bytes", type=int, default=None, help="text bytes per GPU (default: config n)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-report", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--strategy", type=int, default=0)
+    ap.add_argument("--peel", type=int, default=0)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        d = json.load(open(MEASURED_PEAKS))
+        return float(d["hbm_gbs"]), "measured", d
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback", {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- workload
+
+def build_workload(args, rank: int, world: int):
+    import synth
+    cfg = args.config.lower()
+    base = synth.text_spec(cfg)
+    n_shard = args.shard_bytes or base.n
+    N = n_shard * world
+    spec = synth.text_spec(cfg, n=N)
+    lengths = [int(x) for x in args.lengths.split(",")] if args.lengths else None
+    pats = synth.patterns(cfg, spec=spec, per_m=args.per_m, lengths=lengths)
+    return spec, pats
+
+
+# ----------------------------------------------------------------------------- reference arm (CPU oracle)
+
+def cpu_oracle_sample(spec, pats, seconds: float, threads: int):
+    """Oracle (plain Alg. 1) GB/s on the host cores over a bounded sample of the workload.
+
+    Sample: the first min(n, 64 MiB) bytes of the text; patterns taken round-robin over
+    the config's lengths; threads = all host cores (ctypes releases the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle
+    oracle.build()
+    sample_n = min(spec.n, 64 << 20)
+    text = spec.host(0, sample_n)
+    by_m = {}
+    for p in pats:
+        by_m.setdefault(p.m, []).append(p.data)
+    order = []
+    k = 0
+    while len(order) < 4 * threads * 8:
+        for m in sorted(by_m):
+            if k < len(by_m[m]):
+                order.append(by_m[m][k])
+        k += 1
+        if k > max(len(v) for v in by_m.values()):
+            break
+    done_bytes = 0
+    done = 0
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        i = 0
+        while i < len(order) and time.perf_counter() - t0 < seconds:
+            batch = order[i:i + threads]
+            list(ex.map(lambda p: oracle.naive_count(p, text), batch))
+            done_bytes += sample_n * len(batch)
+            done += len(batch)
+            i += threads
+    dt = time.perf_counter() - t0
+    return {
+        "value": done_bytes / dt / 1e9,
+        "unit": "GB/s",
+        "cores": threads,
+        "kind": "oracle",
+        "sample": f"plain Alg. 1 (oracle/oracle.c, gcc -O2) counting {done} patterns of the config's lengths "
+                  f"over the first {sample_n >> 20} MiB of the {spec.name} text, {threads} threads, {dt:.1f} s",
+    }
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    spec, pats = build_workload(args, 0, 1)
+    threads = len(os.sched_getaffinity(0))
+    per_step = max(2.0, args.cpu_seconds / 4)
+    for _ in range(args.warmup):
+        cpu_oracle_sample(spec, pats, 0.5, threads)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        vals.append(cpu_oracle_sample(spec, pats, per_step, threads))
+    total = time.perf_counter() - t0
+    v = sum(x["value"] for x in vals) / len(vals)
+    cb = dict(vals[-1])
+    cb["value"] = v
+    out = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": spec.name, "text_bytes": spec.n, "patterns": len(pats),
+                   "lengths": sorted({p.m for p in pats}), "world": world},
+        "cpu_baseline": cb,
+        "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+# ----------------------------------------------------------------------------- native arm
+
+def run_native(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1612_01506_b200 as sm
+    import synth
+    from paper_1612_01506_b200 import dist as smd
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    sm.load_library()
+    synth.build()
+
+    spec, pats = build_workload(args, rank, world)
+    max_m = max(p.m for p in pats)
+    shard = smd.make_shard(spec.n, rank, world, halo=max(0, max_m - 1))
+    text = synth.gen_text_device(spec, shard.own_lo, shard.held_len)
+    owned = text[: shard.owned_bytes]
+    P = len(pats)
+    pdata = [p.data for p in pats]
+    views = [text[: shard.view_len(p.m)] for p in pats]
+    counts = torch.zeros(P, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream()
+    ev_pairs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(P)]
+
+    def step(record=False):
+        h = smd.global_histogram(text, shard)             # A1 (+ all_reduce)
+        hh = h.cpu().numpy().astype(np.uint64)           # 2 KiB D2H for the host-side order (A2)
+        for i in range(P):
+            if record:
+                ev_pairs[i][0].record(stream)
+            sm.sm_count_async(pdata[i], views[i], counts[i:i + 1], hist=hh, peel=args.peel,
+                              strategy=args.strategy)
+            if record:
+                ev_pairs[i][1].record(stream)
+        smd.allreduce_sum_(counts)
+        return hh
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 1)):
+        hh = step()
+    barrier()
+
+    # ---------------- timed region (device time, max over ranks)
+    clk = ClockSampler(local)
+    clk.start()
+    launches0 = sm.sm_launch_count()
+    kern_ms = np.zeros(P)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    start.record(stream)
+    for s in range(args.steps):
+        step(record=True)
+        if s == args.steps - 1:
+            end.record(stream)
+        torch.cuda.synchronize()
+        kern_ms += np.array([a.elapsed_time(b) for a, b in ev_pairs])
+    barrier()
+    launches = sm.sm_launch_count() - launches0
+    total_ms = start.elapsed_time(end)
+    clocks = clk.stop()
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    bytes_per_step = spec.n * P
+    value = bytes_per_step / (ms_per_step * 1e-3) / 1e9
+
+    # per-kernel roofline (this rank's launches, averaged)
+    kern_ms /= args.steps
+    local_bytes = np.array([v.numel() for v in views], dtype=np.float64)
+    peak, peak_kind, pk = peaks()
+    achieved = float(local_bytes.sum() / (kern_ms.sum() * 1e-3) / 1e9)
+    lens = sorted({p.m for p in pats})
+    per_m = {}
+    for m in lens:
+        idx = [i for i, p in enumerate(pats) if p.m == m]
+        gbs = float(local_bytes[idx].sum() / (kern_ms[idx].sum() * 1e-3) / 1e9)
+        per_m[str(m)] = {"GBps": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4),
+                         "us_per_launch": round(float(kern_ms[idx].mean() * 1e3), 2)}
+    counts_host = counts.cpu().numpy()
+
+    # ---------------- end-to-end through the public API (host text in pinned memory)
+    e2e = None
+    if not args.no_e2e:
+        host_text = torch.empty(text.numel(), dtype=torch.uint8, pin_memory=True)
+        host_text.copy_(text)
+        counts_h = torch.empty(P, dtype=torch.int64, pin_memory=True)
+        text2 = torch.empty_like(text)
+        views2 = [text2[: v.numel()] for v in views]
+
+        def e2e_step():
+            text2.copy_(host_text, non_blocking=True)                    # H2D of the step's input
+            h = smd.global_histogram(text2, shard)
+            hh2 = h.cpu().numpy().astype(np.uint64)
+            for i in range(P):
+                sm.sm_count_async(pdata[i], views2[i], counts[i:i + 1], hist=hh2)
+            smd.allreduce_sum_(counts)
+            counts_h.copy_(counts, non_blocking=True)                    # D2H of the step's result
+        e2e_step()
+        barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        s1.record(stream)
+        barrier()
+        et = torch.tensor([s0.elapsed_time(s1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e_ms = float(et.item()) / args.steps
+        assert np.array_equal(counts_h.numpy(), counts_host), "e2e counts differ from device-resident run"
+        e2e = {"value": bytes_per_step / (e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(text.numel()), "d2h_bytes_per_step": int(8 * P)}
+        del text2, host_text
+
+    # ---------------- reporting (A8), one pass over all patterns, N = 1 only
+    report = None
+    if not args.no_report and world == 1:
+        tot = int(counts_host.sum())
+        posbuf = torch.empty(max(tot, 1), dtype=torch.int64, device=dev)
+        offs = np.concatenate([[0], np.cumsum(counts_host)])
+        dcnt = torch.zeros(P, dtype=torch.int64, device=dev)
+
+        def rep():
+            for i in range(P):
+                sm.sm_report_async(pdata[i], views[i], posbuf[int(offs[i]): int(offs[i + 1])], dcnt[i:i + 1],
+                                   hist=hh)
+        rep()
+        torch.cuda.synchronize()
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0.record(stream)
+        rep()
+        r1.record(stream)
+        torch.cuda.synchronize()
+        r_ms = r0.elapsed_time(r1)
+        assert np.array_equal(dcnt.cpu().numpy(), counts_host), "report totals differ from counts"
+        report = {"value": spec.n * P / (r_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_pass": r_ms,
+                  "positions_written": tot, "position_bytes": 8 * tot}
+        del posbuf
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    cpu = None
+    if not args.no_cpu and world == 1:
+        cpu = cpu_oracle_sample(spec, pats, args.cpu_seconds, len(os.sched_getaffinity(0)))
+
+    strategies = {}
+    for p in pats[:: max(1, P // 200)]:
+        s_, r_ = sm.sm_plan(p.data, hh)
+        key = f"{sm.STRATEGY_NAMES[s_]}/r={r_}"
+        strategies[key] = strategies.get(key, 0) + 1
+
+    out = {
+        "metric": METRIC,
+        "value": round(value, 2),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8",
+        "data": "synthetic",
+        "config": {
+            "workload": spec.name, "text_bytes": spec.n, "text_bytes_per_gpu": shard.owned_bytes,
+            "patterns": P, "lengths": lens, "parallelism": f"text-shard x{world}",
+            "l2": "inputs larger than L2 (256 MiB/GPU vs 126 MB); TMA loads use L2 evict_first",
+            "step": "hist + per-pattern order + count launch per pattern (+ all_reduce)",
+        },
+        "gpu_launches": int(launches),
+        "roofline": {
+            "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": None,
+            "kernel": "search_kernel (count)", "peak_kind": peak_kind,
+            "algorithmic_bytes_per_launch": "n (text bytes of the launch's view)",
+        },
+        "per_m": per_m,
+        "clocks": clocks,
+        "e2e": e2e,
+        "report": report,
+        "cpu_baseline": cpu,
+        "plans": strategies,
+        "count_checksum": int(counts_host.sum()),
+    }
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_native(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,162 @@
+/*
+ * smgpu.h -- C ABI of the B200-native exact string-matching hot path of
+ *   Tarhio, Holub, Giaquinta, "Technology Beats Algorithms (in Exact String
+ *   Matching)", arXiv:1612.01506.
+ *
+ * The problem (Sec. 1): "counting or reporting all the locations
+ * of given pattern p of length m=|p| in given text t of length n=|t|", p and t
+ * strings over a finite alphabet.  Here the alphabet is all 256 byte values;
+ * NUL is an ordinary symbol (reading R15).  The argument order (p, m, t, n)
+ * follows Naive-search(p, m, t, n), PAPER.md:41 (Alg. 1).
+ *
+ * Result definition (Alg. 1; every alignment is visited, so
+ * occurrences overlap, reading R3):
+ *      count = #{ i in [0, n-m] : t[i..i+m) == p }           (0 if n < m)
+ * Positions are 0-based byte offsets (paper position - 1, reading R1),
+ * reported strictly ascending = Alg. 1's loop order.
+ *
+ * Method (Algs. 3-4): pattern positions are compared in
+ * the order pi of increasing frequency of their symbol in the text
+ * (PAPER.md:16,113,138), the first r comparisons unconditionally ("loop
+ * peeling"), blocks of alignments dropped as soon as no
+ * alignment in them survives.  Order, peeling factor and
+ * strategy change the work done, never the result.
+ *
+ * Placement and ownership
+ *   - t, d_hist, d_count, pos: DEVICE memory of the current CUDA device.
+ *     t is checked with cudaPointerGetAttributes; host memory is rejected
+ *     with SM_EINVAL (there is no CPU fallback).
+ *   - p, order, hist: HOST memory, read during the call only (the pattern
+ *     and its order are packed into kernel parameters at launch).
+ *   - The caller owns every buffer; the library keeps no pointer after the
+ *     call returns (async calls: after the enqueued work completes).
+ *   - Scratch comes from the stream-ordered allocator (cudaMallocAsync).
+ *   - stream: a cudaStream_t passed as void*; NULL means cudaStreamPerThread.
+ *
+ * Errors: every call except sm_count returns sm_status and records it (with a
+ * message) in thread-local state readable by sm_last_error()/
+ * sm_last_error_message().  sm_count returns SM_COUNT_ERROR on failure.
+ *   SM_EINVAL  m == 0, m > SM_MAX_PATTERN, NULL p with m > 0, NULL t with n > 0,
+ *              t not device memory, bad strategy/order.
+ *   n < m (including n == 0) is NOT an error: count 0 (reading R2).
+ *   SM_ETRUNC  sm_report found more than cap occurrences (first cap written).
+ *   SM_ECUDA   a CUDA runtime error (message has the CUDA error string).
+ *
+ * Re-entrancy: no global mutable state besides the thread-local error; calls
+ * on different streams may overlap.
+ */
+#ifndef SMGPU_H
+#define SMGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum sm_status {
+  SM_OK = 0,
+  SM_EINVAL = 1,
+  SM_ETRUNC = 2,
+  SM_ENOMEM = 3,
+  SM_ECUDA = 4
+} sm_status;
+
+/* Which device strategy evaluates the remaining comparisons (both exact):
+ *  SM_STRATEGY_FILTER: the first comparison (pi(1), the rarest symbol) is done
+ *     for 16 alignments per lane with packed-byte compares; each surviving
+ *     alignment then runs pi(2..m) with early exit (alpha drops to 1 after
+ *     the peeled block compare).  Best when the rarest symbol is rare.
+ *  SM_STRATEGY_BLOCK: Alg. 4 as written: r peeled packed-byte compares over
+ *     16 alignments per lane, then the pi-ordered loop over the warp's 512
+ *     alignments with a warp-uniform exit test.  Best for
+ *     small alphabets / periodic text.
+ *  SM_STRATEGY_AUTO: chosen on the host from the text histogram. */
+typedef enum sm_strategy {
+  SM_STRATEGY_AUTO = 0,
+  SM_STRATEGY_FILTER = 1,
+  SM_STRATEGY_BLOCK = 2
+} sm_strategy;
+
+#define SM_COUNT_ERROR UINT64_MAX
+#define SM_MAX_PATTERN 4096u
+
+/* ------------------------------------------------------------------------ */
+/* North-star calls (synchronous; run on cudaStreamPerThread)               */
+/* ------------------------------------------------------------------------ */
+
+/* Number of (overlapping) occurrences of p[0..m) in device text t[0..n).
+ * Computes the text histogram and rarest-first order internally.
+ * Returns SM_COUNT_ERROR (and sets sm_last_error) on failure. */
+uint64_t sm_count(const uint8_t* p, size_t m, const uint8_t* t, size_t n);
+
+/* Reporting version ("printing position i"): writes the first
+ * min(count, cap) ascending 0-based positions to DEVICE array pos[0..cap) and
+ * the total count to *count_out (host).  count > cap -> SM_ETRUNC (positions
+ * beyond cap are dropped; *count_out is the total).  Two-call idiom: cap=0. */
+sm_status sm_report(const uint8_t* p, size_t m, const uint8_t* t, size_t n,
+                    uint64_t* pos, size_t cap, uint64_t* count_out);
+
+/* Comparison order pi: order[k] (host, m entries) = 0-based
+ * pattern position compared k-th; positions sorted by ascending count of
+ * their symbol in t (device histogram), ties by ascending position (R11). */
+sm_status sm_symbol_order(const uint8_t* t, size_t n, const uint8_t* p, size_t m,
+                          uint32_t* order);
+
+/* ------------------------------------------------------------------------ */
+/* Building blocks (asynchronous unless stated)                              */
+/* ------------------------------------------------------------------------ */
+
+/* d_hist[c] = #{x in [0,n) : t[x] = c}, c = 0..255 (DEVICE u64[256],
+ * overwritten).  Async on `stream`.  PAPER.md:16,113 (frequencies in the text). */
+sm_status sm_histogram(const uint8_t* t, size_t n, uint64_t* d_hist, void* stream);
+
+/* Host-only: stable rarest-first order from a host histogram. */
+sm_status sm_order_from_histogram(const uint64_t* hist, const uint8_t* p, size_t m,
+                                  uint32_t* order);
+
+/* Enqueue the count of p in t on `stream`; the result lands in *d_count
+ * (DEVICE u64, overwritten).
+ *   hist     host u64[256] symbol counts of t (for order and strategy);
+ *            NULL -> computed on the device (synchronises `stream`).
+ *   order    host u32[m] comparison order (any permutation of 0..m-1);
+ *            NULL -> rarest-first from hist.
+ *   peel     peeling factor r >= 1 (clamped to m, reading R9); 0 -> auto.
+ *   strategy sm_strategy. */
+sm_status sm_count_async(const uint8_t* p, size_t m, const uint8_t* t, size_t n,
+                         const uint64_t* hist, const uint32_t* order, uint32_t peel,
+                         int strategy, uint64_t* d_count, void* stream);
+
+/* Enqueue the reporting version: the first min(count, cap) ascending
+ * positions go to DEVICE pos[0..cap), the total count to DEVICE *d_count.
+ * Truncation is detected by the caller (*d_count > cap) after the stream
+ * synchronises.  Same hist/order/peel/strategy meaning as sm_count_async. */
+sm_status sm_report_async(const uint8_t* p, size_t m, const uint8_t* t, size_t n,
+                          const uint64_t* hist, const uint32_t* order, uint32_t peel,
+                          int strategy, uint64_t* pos, size_t cap, uint64_t* d_count,
+                          void* stream);
+
+/* Plan introspection (host-only, no GPU work): the strategy and peeling
+ * factor sm_count_async would pick for (p, hist, order).  Used by tests and
+ * the benchmark to label measurements. */
+sm_status sm_plan(const uint8_t* p, size_t m, const uint64_t* hist, const uint32_t* order,
+                  uint32_t peel, int strategy, int* strategy_out, uint32_t* peel_out);
+
+/* Thread-local status of the last failing call on this thread (SM_OK if none
+ * since sm_clear_error), its message, and a static name for a status. */
+sm_status sm_last_error(void);
+const char* sm_last_error_message(void);
+void sm_clear_error(void);
+const char* sm_status_string(sm_status s);
+
+/* Library version string and the number of kernels the library has launched
+ * on this thread (for the benchmark's gpu_launches claim). */
+const char* sm_version(void);
+uint64_t sm_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SMGPU_H */

@@ -1,0 +1,283 @@
+"""B200-native exact string matching (arXiv:1612.01506 hot path) -- Python binding.
+
+Thin ctypes marshalling over the C ABI in ``include/smgpu.h`` (libsmgpu.so,
+built in-tree for sm_100a).  Every step of the path on the text runs in the
+library's CUDA kernels; this module only converts arguments.  There is no CPU
+fallback: if the library or a CUDA device is missing, calls raise.
+
+Names mirror the ABI:
+
+* ``sm_count(p, t)``                      -> int
+* ``sm_report(p, t, cap=None)``           -> (positions int64 CUDA tensor, total)
+* ``sm_symbol_order(t, p)``               -> list[int]   (0-based pi)
+* ``sm_histogram(t, out=None)``           -> int64[256] CUDA tensor (async)
+* ``sm_order_from_histogram(hist, p)``    -> list[int]
+* ``sm_count_async(p, t, d_count, ...)``  -> None (enqueued on the current stream)
+* ``sm_report_async(p, t, pos, d_count, ...)``
+* ``sm_plan(p, hist, ...)``               -> (strategy, peel)
+
+``t`` is a 1-D contiguous ``torch.uint8`` CUDA tensor (any storage offset).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsmgpu.so")
+
+SM_OK, SM_EINVAL, SM_ETRUNC, SM_ENOMEM, SM_ECUDA = 0, 1, 2, 3, 4
+SM_STRATEGY_AUTO, SM_STRATEGY_FILTER, SM_STRATEGY_BLOCK = 0, 1, 2
+SM_COUNT_ERROR = (1 << 64) - 1
+SM_MAX_PATTERN = 4096
+STRATEGY_NAMES = {SM_STRATEGY_FILTER: "filter", SM_STRATEGY_BLOCK: "block"}
+
+EXPORTED_SYMBOLS = (
+    "sm_count", "sm_report", "sm_symbol_order", "sm_histogram", "sm_order_from_histogram",
+    "sm_count_async", "sm_report_async", "sm_plan", "sm_last_error", "sm_last_error_message",
+    "sm_clear_error", "sm_status_string", "sm_version", "sm_launch_count",
+)
+
+
+class SmError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{_status_name(status)}: {message}")
+        self.status = status
+
+
+def _status_name(s: int) -> str:
+    return {0: "SM_OK", 1: "SM_EINVAL", 2: "SM_ETRUNC", 3: "SM_ENOMEM", 4: "SM_ECUDA"}.get(s, f"SM_{s}")
+
+
+_lib = None
+_u8p = ctypes.c_void_p
+_vp = ctypes.c_void_p
+_sz = ctypes.c_size_t
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libsmgpu.so (raises if it has not been built -- no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    lib.sm_count.restype = ctypes.c_uint64
+    lib.sm_count.argtypes = [_u8p, _sz, _u8p, _sz]
+    lib.sm_report.restype = ctypes.c_int
+    lib.sm_report.argtypes = [_u8p, _sz, _u8p, _sz, _vp, _sz, ctypes.POINTER(ctypes.c_uint64)]
+    lib.sm_symbol_order.restype = ctypes.c_int
+    lib.sm_symbol_order.argtypes = [_u8p, _sz, _u8p, _sz, _vp]
+    lib.sm_histogram.restype = ctypes.c_int
+    lib.sm_histogram.argtypes = [_u8p, _sz, _vp, _vp]
+    lib.sm_order_from_histogram.restype = ctypes.c_int
+    lib.sm_order_from_histogram.argtypes = [_vp, _u8p, _sz, _vp]
+    lib.sm_count_async.restype = ctypes.c_int
+    lib.sm_count_async.argtypes = [_u8p, _sz, _u8p, _sz, _vp, _vp, ctypes.c_uint32, ctypes.c_int, _vp, _vp]
+    lib.sm_report_async.restype = ctypes.c_int
+    lib.sm_report_async.argtypes = [_u8p, _sz, _u8p, _sz, _vp, _vp, ctypes.c_uint32, ctypes.c_int, _vp, _sz,
+                                    _vp, _vp]
+    lib.sm_plan.restype = ctypes.c_int
+    lib.sm_plan.argtypes = [_u8p, _sz, _vp, _vp, ctypes.c_uint32, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                            ctypes.POINTER(ctypes.c_uint32)]
+    lib.sm_last_error.restype = ctypes.c_int
+    lib.sm_last_error.argtypes = []
+    lib.sm_last_error_message.restype = ctypes.c_char_p
+    lib.sm_last_error_message.argtypes = []
+    lib.sm_clear_error.restype = None
+    lib.sm_clear_error.argtypes = []
+    lib.sm_status_string.restype = ctypes.c_char_p
+    lib.sm_status_string.argtypes = [ctypes.c_int]
+    lib.sm_version.restype = ctypes.c_char_p
+    lib.sm_version.argtypes = []
+    lib.sm_launch_count.restype = ctypes.c_uint64
+    lib.sm_launch_count.argtypes = []
+    _lib = lib
+    return lib
+
+
+def _raise(status: int):
+    lib = load_library()
+    raise SmError(status, lib.sm_last_error_message().decode(errors="replace"))
+
+
+def _pattern(p) -> Tuple[ctypes.Array, int]:
+    if isinstance(p, str):
+        p = p.encode("latin-1")
+    b = bytes(p) if not isinstance(p, np.ndarray) else np.ascontiguousarray(p, dtype=np.uint8).tobytes()
+    buf = ctypes.create_string_buffer(b, max(len(b), 1))
+    return buf, len(b)
+
+
+def _text(t) -> Tuple[int, int]:
+    """(device pointer, n) of a 1-D contiguous uint8 CUDA tensor."""
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError("t must be a torch.uint8 CUDA tensor (device-resident text)")
+    if t.dtype != torch.uint8 or t.dim() != 1 or not t.is_contiguous():
+        raise TypeError("t must be a 1-D contiguous torch.uint8 tensor")
+    return t.data_ptr(), t.numel()
+
+
+def _stream(stream) -> int:
+    import torch
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _u64_host(a) -> Optional[np.ndarray]:
+    if a is None:
+        return None
+    if hasattr(a, "detach"):
+        a = a.detach().cpu().numpy()
+    return np.ascontiguousarray(np.asarray(a).astype(np.uint64))
+
+
+def _u32_host(a) -> Optional[np.ndarray]:
+    if a is None:
+        return None
+    return np.ascontiguousarray(np.asarray(a, dtype=np.uint32))
+
+
+def _np_ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data
+
+
+# ----------------------------------------------------------------------------- north-star calls
+
+def sm_count(p, t) -> int:
+    """Number of overlapping occurrences of p in the device text t."""
+    lib = load_library()
+    pb, m = _pattern(p)
+    tp, n = _text(t)
+    import torch
+    torch.cuda.current_stream().synchronize()  # text produced on torch's stream must be ready
+    r = lib.sm_count(pb, m, tp, n)
+    if r == SM_COUNT_ERROR:
+        _raise(lib.sm_last_error())
+    return int(r)
+
+
+def sm_report(p, t, cap: Optional[int] = None):
+    """Ascending 0-based positions.  Returns (positions, total).
+
+    cap=None: two-call idiom, all positions returned.  With a cap smaller than
+    the total the first `cap` positions are returned and total > len(positions).
+    """
+    import torch
+    lib = load_library()
+    pb, m = _pattern(p)
+    tp, n = _text(t)
+    torch.cuda.current_stream().synchronize()
+    cnt = ctypes.c_uint64(0)
+    if cap is None:
+        s = lib.sm_report(pb, m, tp, n, None, 0, ctypes.byref(cnt))
+        if s not in (SM_OK, SM_ETRUNC):
+            _raise(s)
+        cap = int(cnt.value)
+    pos = torch.empty(max(cap, 1), dtype=torch.int64, device=t.device)
+    s = lib.sm_report(pb, m, tp, n, pos.data_ptr() if cap > 0 else None, cap, ctypes.byref(cnt))
+    if s not in (SM_OK, SM_ETRUNC):
+        _raise(s)
+    total = int(cnt.value)
+    return pos[: min(total, cap)], total
+
+
+def sm_symbol_order(t, p) -> list:
+    """Rarest-first comparison order pi from the device histogram of t."""
+    import torch
+    lib = load_library()
+    pb, m = _pattern(p)
+    tp, n = _text(t)
+    torch.cuda.current_stream().synchronize()
+    out = np.zeros(max(m, 1), dtype=np.uint32)
+    s = lib.sm_symbol_order(tp, n, pb, m, out.ctypes.data)
+    if s != SM_OK:
+        _raise(s)
+    return out[:m].tolist()
+
+
+# ----------------------------------------------------------------------------- building blocks
+
+def sm_histogram(t, out=None, stream=None):
+    """Device byte histogram of t into an int64[256] CUDA tensor (async on `stream`)."""
+    import torch
+    lib = load_library()
+    tp, n = _text(t)
+    if out is None:
+        out = torch.empty(256, dtype=torch.int64, device=t.device)
+    s = lib.sm_histogram(tp, n, out.data_ptr(), _stream(stream))
+    if s != SM_OK:
+        _raise(s)
+    return out
+
+
+def sm_order_from_histogram(hist, p) -> list:
+    lib = load_library()
+    h = _u64_host(hist)
+    pb, m = _pattern(p)
+    out = np.zeros(max(m, 1), dtype=np.uint32)
+    s = lib.sm_order_from_histogram(h.ctypes.data, pb, m, out.ctypes.data)
+    if s != SM_OK:
+        _raise(s)
+    return out[:m].tolist()
+
+
+def sm_count_async(p, t, d_count, hist=None, order: Optional[Sequence[int]] = None, peel: int = 0,
+                   strategy: int = SM_STRATEGY_AUTO, stream=None) -> None:
+    """Enqueue the count of p in t into the 1-element int64 CUDA tensor (or pointer) d_count."""
+    lib = load_library()
+    pb, m = _pattern(p)
+    tp, n = _text(t)
+    h, o = _u64_host(hist), _u32_host(order)
+    dptr = d_count if isinstance(d_count, int) else d_count.data_ptr()
+    s = lib.sm_count_async(pb, m, tp, n, _np_ptr(h), _np_ptr(o), peel, strategy, dptr, _stream(stream))
+    if s != SM_OK:
+        _raise(s)
+
+
+def sm_report_async(p, t, pos, d_count, hist=None, order: Optional[Sequence[int]] = None, peel: int = 0,
+                    strategy: int = SM_STRATEGY_AUTO, stream=None) -> None:
+    """Enqueue reporting: first min(count, pos.numel()) positions into pos, total into d_count."""
+    lib = load_library()
+    pb, m = _pattern(p)
+    tp, n = _text(t)
+    h, o = _u64_host(hist), _u32_host(order)
+    cap = 0 if pos is None else pos.numel()
+    pptr = None if pos is None else pos.data_ptr()
+    dptr = d_count if isinstance(d_count, int) else d_count.data_ptr()
+    s = lib.sm_report_async(pb, m, tp, n, _np_ptr(h), _np_ptr(o), peel, strategy, pptr, cap, dptr,
+                            _stream(stream))
+    if s != SM_OK:
+        _raise(s)
+
+
+def sm_plan(p, hist, order=None, peel: int = 0, strategy: int = SM_STRATEGY_AUTO) -> Tuple[int, int]:
+    lib = load_library()
+    pb, m = _pattern(p)
+    h, o = _u64_host(hist), _u32_host(order)
+    so, ro = ctypes.c_int(0), ctypes.c_uint32(0)
+    s = lib.sm_plan(pb, m, _np_ptr(h), _np_ptr(o), peel, strategy, ctypes.byref(so), ctypes.byref(ro))
+    if s != SM_OK:
+        _raise(s)
+    return int(so.value), int(ro.value)
+
+
+def sm_last_error() -> Tuple[int, str]:
+    lib = load_library()
+    return int(lib.sm_last_error()), lib.sm_last_error_message().decode(errors="replace")
+
+
+def sm_launch_count() -> int:
+    return int(load_library().sm_launch_count())
+
+
+def sm_version() -> str:
+    return load_library().sm_version().decode()

@@ -1,0 +1,440 @@
+// abi.cu -- the C ABI (include/smgpu.h): argument checking, planning (order pi,
+// peeling factor r, strategy, tiling) and launch orchestration.  Host code only;
+// every step of the path on the text runs in the kernels of this library.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "launch.h"
+#include "smgpu.h"
+
+using namespace smgpu;
+
+namespace {
+
+thread_local sm_status g_status = SM_OK;
+thread_local std::string g_message;
+thread_local uint64_t g_launches = 0;
+
+sm_status fail(sm_status s, const std::string& msg) {
+  g_status = s;
+  g_message = msg;
+  return s;
+}
+
+sm_status cuda_fail(cudaError_t e, const char* what) {
+  std::string msg = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  return fail(e == cudaErrorMemoryAllocation ? SM_ENOMEM : SM_ECUDA, msg);
+}
+
+#define SM_CUDA_TRY(expr, what)                      \
+  do {                                               \
+    cudaError_t _e = (expr);                         \
+    if (_e != cudaSuccess) return cuda_fail(_e, what); \
+  } while (0)
+
+int num_sms() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  static int cache[64] = {0};
+  if (dev < 64 && cache[dev]) return cache[dev];
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (dev < 64) cache[dev] = sms;
+  return sms;
+}
+
+cudaStream_t as_stream(void* s) { return s ? reinterpret_cast<cudaStream_t>(s) : cudaStreamPerThread; }
+
+sm_status check_device_ptr(const void* ptr, const char* name) {
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(SM_EINVAL, std::string(name) + " is not a CUDA-visible pointer");
+  }
+  if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)
+    return fail(SM_EINVAL, std::string(name) + " must be device memory (no CPU fallback)");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (at.type == cudaMemoryTypeDevice && at.device != dev)
+    return fail(SM_EINVAL, std::string(name) + " lives on another device than the current one");
+  return SM_OK;
+}
+
+sm_status check_pattern_text(const uint8_t* p, size_t m, const uint8_t* t, size_t n) {
+  if (m == 0) return fail(SM_EINVAL, "m == 0: empty pattern is undefined (reading R2)");
+  if (m > SM_MAX_PATTERN) return fail(SM_EINVAL, "m > SM_MAX_PATTERN (4096)");
+  if (!p) return fail(SM_EINVAL, "p is NULL");
+  if (n > 0) {
+    if (!t) return fail(SM_EINVAL, "t is NULL with n > 0");
+    sm_status s = check_device_ptr(t, "t");
+    if (s != SM_OK) return s;
+  }
+  return SM_OK;
+}
+
+// stable rarest-first order (ties by position, R11)
+void order_from_hist(const uint64_t* hist, const uint8_t* p, size_t m, uint32_t* order) {
+  std::vector<uint32_t> idx(m);
+  for (size_t j = 0; j < m; ++j) idx[j] = (uint32_t)j;
+  std::stable_sort(idx.begin(), idx.end(), [&](uint32_t a, uint32_t b) { return hist[p[a]] < hist[p[b]]; });
+  std::memcpy(order, idx.data(), m * sizeof(uint32_t));
+}
+
+bool valid_permutation(const uint32_t* order, size_t m) {
+  std::vector<char> seen(m, 0);
+  for (size_t k = 0; k < m; ++k) {
+    if (order[k] >= m || seen[order[k]]) return false;
+    seen[order[k]] = 1;
+  }
+  return true;
+}
+
+constexpr double kFilterMaxF = 0.10;  // FILTER when the rarest pattern symbol has freq <= this
+
+struct Plan {
+  int strategy = kFilter;
+  uint32_t r = 1;
+  int cpl = 4;
+  uint32_t tile = 16384;
+  std::vector<uint32_t> order;
+};
+
+void choose_tiling(uint64_t n, Plan& pl) {
+  const uint64_t sms = (uint64_t)num_sms();
+  pl.tile = 16384;
+  pl.cpl = 4;
+  if ((n + pl.tile - 1) / pl.tile < 2 * sms) {
+    pl.tile = 4096;
+    pl.cpl = 1;
+  }
+}
+
+sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist, const uint32_t* order,
+                    uint32_t peel, int strategy, Plan& pl) {
+  if (strategy < SM_STRATEGY_AUTO || strategy > SM_STRATEGY_BLOCK) return fail(SM_EINVAL, "bad strategy");
+  pl.order.resize(m);
+  if (order) {
+    if (!valid_permutation(order, m)) return fail(SM_EINVAL, "order is not a permutation of 0..m-1");
+    std::memcpy(pl.order.data(), order, m * sizeof(uint32_t));
+  } else {
+    order_from_hist(hist, p, m, pl.order.data());
+  }
+  choose_tiling(n, pl);
+  double total = 0;
+  for (int c = 0; c < 256; ++c) total += (double)hist[c];
+  auto freq = [&](size_t k) { return total > 0 ? (double)hist[p[pl.order[k]]] / total : 0.0; };
+  if (strategy == SM_STRATEGY_AUTO) strategy = freq(0) <= kFilterMaxF ? kFilter : kBlock;
+  pl.strategy = strategy;
+  if (peel == 0) {
+    // smallest r with alpha_eff * prod_{k<r} f(pi(k)) <= 1/2 (PAPER.md:176-178 reasoning at alpha_eff)
+    double surv = 32.0 * 16.0 * pl.cpl;
+    uint32_t r = 0;
+    while (r < m && surv > 0.5) surv *= freq(r++);
+    peel = r < 1 ? 1 : r;
+  }
+  pl.r = std::min<uint32_t>(peel, (uint32_t)m);
+  if (pl.strategy == kFilter) pl.r = 1;
+  return SM_OK;
+}
+
+sm_status host_hist(const uint8_t* t, size_t n, cudaStream_t st, uint64_t* out) {
+  uint64_t* d = nullptr;
+  SM_CUDA_TRY(cudaMallocAsync(&d, 256 * sizeof(uint64_t), st), "cudaMallocAsync(hist)");
+  cudaError_t e = launch_hist(t, n, d, num_sms(), st);
+  if (e == cudaSuccess) {
+    ++g_launches;
+    e = cudaMemcpyAsync(out, d, 256 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
+  }
+  cudaFreeAsync(d, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "histogram");
+  return SM_OK;
+}
+
+// Fill the launch description for plan `pl`.
+void make_args(const Plan& pl, const uint8_t* p, size_t m, const uint8_t* t, size_t n, SearchArgs& a,
+               std::vector<uint32_t>& table, int& grid, size_t& smem) {
+  std::memset(&a, 0, sizeof(a));
+  const uintptr_t tp = reinterpret_cast<uintptr_t>(t);
+  a.base = reinterpret_cast<const uint8_t*>(tp & ~(uintptr_t)15);
+  a.delta = tp & 15;
+  a.n = n;
+  a.A = n - m + 1;
+  a.m = (uint32_t)m;
+  a.r = pl.r;
+  a.tile = pl.tile;
+  const uint64_t T = pl.tile;
+  table.resize(m);
+  for (size_t k = 0; k < m; ++k) table[k] = pl.order[k] | ((uint32_t)p[pl.order[k]] << 16);
+  if (pl.strategy == kFilter) {
+    const uint32_t a1 = pl.order[0];
+    a.a1 = a1;
+    a.bc1 = (uint32_t)p[a1] * 0x01010101u;
+    a.pre = (a1 + 15) & ~15u;
+    const uint32_t post = ((uint32_t)(m - 1 - a1) + 15) & ~15u;
+    a.stage_len = (uint32_t)T + a.pre + post;
+    a.k_begin = (a.delta + a1) / T;
+    const uint64_t k_end = (a.delta + a.A - 1 + a1) / T + 1;
+    a.ntiles = k_end - a.k_begin;
+  } else {
+    a.pre = 0;
+    const uint32_t post = (((uint32_t)m - 1) & ~15u) + 16;
+    a.stage_len = (uint32_t)T + post;
+    a.k_begin = 0;
+    a.ntiles = (a.delta + a.A - 1) / T + 1;
+  }
+  a.stage_stride = (a.stage_len + 127) & ~127u;
+  a.tbl_off = 2 * kMaxStages * 8 + 2 * 4 * kConsumerWarps * 4;  // barriers + write-epilogue scratch
+  a.ring_off = (a.tbl_off + 4 * (uint32_t)m + 127) & ~127u;
+  const uint32_t budget = 227 * 1024;
+  uint32_t stages = (budget - a.ring_off) / a.stage_stride;
+  a.stages = std::min<uint32_t>(stages, kMaxStages);
+  smem = (size_t)a.ring_off + (size_t)a.stages * a.stage_stride;
+  const uint64_t sms = (uint64_t)num_sms();
+  grid = (int)std::min<uint64_t>(a.ntiles, sms);
+  if (grid < 1) grid = 1;
+}
+
+sm_status prepare(const uint8_t* p, size_t m, const uint8_t* t, size_t n, const uint64_t* hist,
+                  const uint32_t* order, uint32_t peel, int strategy, cudaStream_t st, Plan& pl,
+                  uint64_t* hist_buf) {
+  const uint64_t* h = hist;
+  if (!h) {
+    sm_status s = host_hist(t, n, st, hist_buf);
+    if (s != SM_OK) return s;
+    h = hist_buf;
+  }
+  return make_plan(p, m, n, h, order, peel, strategy, pl);
+}
+
+sm_status enqueue_count(const uint8_t* p, size_t m, const uint8_t* t, size_t n, const uint64_t* hist,
+                        const uint32_t* order, uint32_t peel, int strategy, uint64_t* d_count, cudaStream_t st) {
+  SM_CUDA_TRY(cudaMemsetAsync(d_count, 0, sizeof(uint64_t), st), "cudaMemsetAsync(count)");
+  if (n < m) return SM_OK;  // reading R2: zero alignments
+  Plan pl;
+  uint64_t hb[256];
+  sm_status s = prepare(p, m, t, n, hist, order, peel, strategy, st, pl, hb);
+  if (s != SM_OK) return s;
+  SearchArgs a;
+  std::vector<uint32_t> table;
+  int grid;
+  size_t smem;
+  make_args(pl, p, m, t, n, a, table, grid, smem);
+  a.count_out = d_count;
+  SM_CUDA_TRY(launch_search(a, table.data(), pl.strategy, kEpiCount, pl.cpl, grid, smem, st), "search kernel");
+  ++g_launches;
+  return SM_OK;
+}
+
+sm_status enqueue_report(const uint8_t* p, size_t m, const uint8_t* t, size_t n, const uint64_t* hist,
+                         const uint32_t* order, uint32_t peel, int strategy, uint64_t* pos, size_t cap,
+                         uint64_t* d_count, cudaStream_t st) {
+  SM_CUDA_TRY(cudaMemsetAsync(d_count, 0, sizeof(uint64_t), st), "cudaMemsetAsync(count)");
+  if (n < m) return SM_OK;
+  Plan pl;
+  uint64_t hb[256];
+  sm_status s = prepare(p, m, t, n, hist, order, peel, strategy, st, pl, hb);
+  if (s != SM_OK) return s;
+  SearchArgs a;
+  std::vector<uint32_t> table;
+  int grid;
+  size_t smem;
+  make_args(pl, p, m, t, n, a, table, grid, smem);
+
+  // scratch: per-tile counts (ntiles + 1, last = 0) and their exclusive prefix
+  const uint64_t nt1 = a.ntiles + 1;
+  size_t temp_bytes = 0;
+  SM_CUDA_TRY(exclusive_scan_u64(nullptr, nullptr, nt1, nullptr, &temp_bytes, st), "scan sizing");
+  const size_t off_bytes = ((nt1 * 8 + 255) / 256) * 256;
+  uint8_t* scratch = nullptr;
+  SM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&scratch), 2 * off_bytes + temp_bytes, st),
+              "cudaMallocAsync(report scratch)");
+  uint64_t* counts = reinterpret_cast<uint64_t*>(scratch);
+  uint64_t* offsets = reinterpret_cast<uint64_t*>(scratch + off_bytes);
+  void* temp = scratch + 2 * off_bytes;
+  cudaError_t e = cudaMemsetAsync(counts, 0, nt1 * 8, st);
+  if (e == cudaSuccess) {
+    a.tile_counts = counts;
+    e = launch_search(a, table.data(), pl.strategy, kEpiTileCount, pl.cpl, grid, smem, st);  // pass 1
+    if (e == cudaSuccess) ++g_launches;
+  }
+  if (e == cudaSuccess) {
+    e = exclusive_scan_u64(counts, offsets, nt1, temp, &temp_bytes, st);
+    if (e == cudaSuccess) g_launches += 1;
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_count, offsets + a.ntiles, 8, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess && cap > 0) {
+    a.tile_counts = nullptr;
+    a.tile_offsets = offsets;
+    a.pos = pos;
+    a.cap = cap;
+    e = launch_search(a, table.data(), pl.strategy, kEpiWrite, pl.cpl, grid, smem, st);  // pass 2
+    if (e == cudaSuccess) ++g_launches;
+  }
+  cudaFreeAsync(scratch, st);
+  if (e != cudaSuccess) return cuda_fail(e, "report");
+  return SM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+uint64_t sm_count(const uint8_t* p, size_t m, const uint8_t* t, size_t n) {
+  if (check_pattern_text(p, m, t, n) != SM_OK) return SM_COUNT_ERROR;
+  if (n < m) return 0;
+  cudaStream_t st = cudaStreamPerThread;
+  uint64_t* d = nullptr;
+  cudaError_t e = cudaMallocAsync(&d, sizeof(uint64_t), st);
+  if (e != cudaSuccess) {
+    cuda_fail(e, "cudaMallocAsync(count)");
+    return SM_COUNT_ERROR;
+  }
+  sm_status s = enqueue_count(p, m, t, n, nullptr, nullptr, 0, SM_STRATEGY_AUTO, d, st);
+  uint64_t h = SM_COUNT_ERROR;
+  if (s == SM_OK) {
+    e = cudaMemcpyAsync(&h, d, sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      cuda_fail(e, "sm_count");
+      h = SM_COUNT_ERROR;
+    }
+  }
+  cudaFreeAsync(d, st);
+  cudaStreamSynchronize(st);
+  return s == SM_OK ? h : SM_COUNT_ERROR;
+}
+
+sm_status sm_report(const uint8_t* p, size_t m, const uint8_t* t, size_t n, uint64_t* pos, size_t cap,
+                    uint64_t* count_out) {
+  sm_status s = check_pattern_text(p, m, t, n);
+  if (s != SM_OK) return s;
+  if (!count_out) return fail(SM_EINVAL, "count_out is NULL");
+  if (cap > 0) {
+    if (!pos) return fail(SM_EINVAL, "pos is NULL with cap > 0");
+    s = check_device_ptr(pos, "pos");
+    if (s != SM_OK) return s;
+  }
+  *count_out = 0;
+  if (n < m) return SM_OK;
+  cudaStream_t st = cudaStreamPerThread;
+  uint64_t* d = nullptr;
+  SM_CUDA_TRY(cudaMallocAsync(&d, sizeof(uint64_t), st), "cudaMallocAsync(count)");
+  s = enqueue_report(p, m, t, n, nullptr, nullptr, 0, SM_STRATEGY_AUTO, pos, cap, d, st);
+  uint64_t h = 0;
+  cudaError_t e = cudaSuccess;
+  if (s == SM_OK) {
+    e = cudaMemcpyAsync(&h, d, sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  }
+  cudaFreeAsync(d, st);
+  cudaStreamSynchronize(st);
+  if (s != SM_OK) return s;
+  if (e != cudaSuccess) return cuda_fail(e, "sm_report");
+  *count_out = h;
+  if (h > cap) return fail(SM_ETRUNC, "more occurrences than cap; first cap positions written");
+  return SM_OK;
+}
+
+sm_status sm_symbol_order(const uint8_t* t, size_t n, const uint8_t* p, size_t m, uint32_t* order) {
+  sm_status s = check_pattern_text(p, m, t, n);
+  if (s != SM_OK) return s;
+  if (!order) return fail(SM_EINVAL, "order is NULL");
+  uint64_t hb[256];
+  if (n > 0) {
+    s = host_hist(t, n, cudaStreamPerThread, hb);
+    if (s != SM_OK) return s;
+  } else {
+    std::memset(hb, 0, sizeof(hb));
+  }
+  order_from_hist(hb, p, m, order);
+  return SM_OK;
+}
+
+sm_status sm_histogram(const uint8_t* t, size_t n, uint64_t* d_hist, void* stream) {
+  if (!d_hist) return fail(SM_EINVAL, "d_hist is NULL");
+  sm_status s = check_device_ptr(d_hist, "d_hist");
+  if (s != SM_OK) return s;
+  if (n > 0) {
+    if (!t) return fail(SM_EINVAL, "t is NULL with n > 0");
+    s = check_device_ptr(t, "t");
+    if (s != SM_OK) return s;
+  }
+  SM_CUDA_TRY(launch_hist(t, n, d_hist, num_sms(), as_stream(stream)), "histogram kernel");
+  if (n > 0) ++g_launches;
+  return SM_OK;
+}
+
+sm_status sm_order_from_histogram(const uint64_t* hist, const uint8_t* p, size_t m, uint32_t* order) {
+  if (m == 0) return fail(SM_EINVAL, "m == 0");
+  if (!hist || !p || !order) return fail(SM_EINVAL, "NULL argument");
+  order_from_hist(hist, p, m, order);
+  return SM_OK;
+}
+
+sm_status sm_count_async(const uint8_t* p, size_t m, const uint8_t* t, size_t n, const uint64_t* hist,
+                         const uint32_t* order, uint32_t peel, int strategy, uint64_t* d_count, void* stream) {
+  sm_status s = check_pattern_text(p, m, t, n);
+  if (s != SM_OK) return s;
+  if (!d_count) return fail(SM_EINVAL, "d_count is NULL");
+  s = check_device_ptr(d_count, "d_count");
+  if (s != SM_OK) return s;
+  return enqueue_count(p, m, t, n, hist, order, peel, strategy, d_count, as_stream(stream));
+}
+
+sm_status sm_report_async(const uint8_t* p, size_t m, const uint8_t* t, size_t n, const uint64_t* hist,
+                          const uint32_t* order, uint32_t peel, int strategy, uint64_t* pos, size_t cap,
+                          uint64_t* d_count, void* stream) {
+  sm_status s = check_pattern_text(p, m, t, n);
+  if (s != SM_OK) return s;
+  if (!d_count) return fail(SM_EINVAL, "d_count is NULL");
+  s = check_device_ptr(d_count, "d_count");
+  if (s != SM_OK) return s;
+  if (cap > 0) {
+    if (!pos) return fail(SM_EINVAL, "pos is NULL with cap > 0");
+    s = check_device_ptr(pos, "pos");
+    if (s != SM_OK) return s;
+  }
+  return enqueue_report(p, m, t, n, hist, order, peel, strategy, pos, cap, d_count, as_stream(stream));
+}
+
+sm_status sm_plan(const uint8_t* p, size_t m, const uint64_t* hist, const uint32_t* order, uint32_t peel,
+                  int strategy, int* strategy_out, uint32_t* peel_out) {
+  if (m == 0 || m > SM_MAX_PATTERN || !p || !hist) return fail(SM_EINVAL, "bad arguments to sm_plan");
+  uint64_t n = 0;
+  for (int c = 0; c < 256; ++c) n += hist[c];
+  Plan pl;
+  sm_status s = make_plan(p, m, n, hist, order, peel, strategy, pl);
+  if (s != SM_OK) return s;
+  if (strategy_out) *strategy_out = pl.strategy;
+  if (peel_out) *peel_out = pl.r;
+  return SM_OK;
+}
+
+sm_status sm_last_error(void) { return g_status; }
+const char* sm_last_error_message(void) { return g_message.c_str(); }
+void sm_clear_error(void) {
+  g_status = SM_OK;
+  g_message.clear();
+}
+
+const char* sm_status_string(sm_status s) {
+  switch (s) {
+    case SM_OK: return "SM_OK";
+    case SM_EINVAL: return "SM_EINVAL";
+    case SM_ETRUNC: return "SM_ETRUNC";
+    case SM_ENOMEM: return "SM_ENOMEM";
+    case SM_ECUDA: return "SM_ECUDA";
+  }
+  return "SM_UNKNOWN";
+}
+
+const char* sm_version(void) { return "smgpu 0.1 (sm_100a)"; }
+uint64_t sm_launch_count(void) { return g_launches; }
+
+}  // extern "C"

@@ -1,0 +1,50 @@
+// search.cuh -- kernel-side description of one search launch.
+#pragma once
+#include <cstdint>
+
+namespace smgpu {
+
+constexpr int kConsumerWarps = 8;                        // warps comparing text
+constexpr int kThreads = (kConsumerWarps + 1) * 32;      // + 1 TMA producer warp
+constexpr int kChunk = 16;                               // alignments per lane-chunk
+constexpr int kLanesPerTilePass = kConsumerWarps * 32;   // lanes sharing a tile
+constexpr int kMaxStages = 8;
+
+enum Strategy : int { kFilter = 1, kBlock = 2 };
+enum Epilogue : int { kEpiCount = 0, kEpiTileCount = 1, kEpiWrite = 2 };
+
+// Everything about a launch except the pattern table.  All byte offsets are
+// relative to `base` = align_down(t, 16); the text occupies offsets
+// [delta, delta + n).  Alignment offset x <-> 0-based position x - delta.
+struct SearchArgs {
+  const uint8_t* base;
+  uint64_t delta;         // t - base (0..15)
+  uint64_t n;             // text length
+  uint64_t A;             // number of alignments, n - m + 1  (n >= m)
+  uint64_t k_begin;       // first tile index (tile k covers [kT, kT+T) in its space)
+  uint64_t ntiles;        // tiles k_begin .. k_begin + ntiles - 1
+  uint32_t m;
+  uint32_t r;             // peeling factor (block strategy), 1 <= r <= m
+  uint32_t a1;            // pattern offset of pi(1)       (filter strategy)
+  uint32_t bc1;           // p[pi(1)] * 0x01010101          (filter strategy)
+  uint32_t tile;          // T, multiple of 16 * kLanesPerTilePass
+  uint32_t pre;           // buffer bytes before the tile (multiple of 16)
+  uint32_t stage_len;     // bytes a stage holds = T + pre + post (multiple of 16)
+  uint32_t stage_stride;  // smem stride between stages (multiple of 128)
+  uint32_t stages;        // ring depth
+  uint32_t tbl_off;       // smem byte offset of the pattern table
+  uint32_t ring_off;      // smem byte offset of stage 0
+  uint64_t* count_out;    // kEpiCount: device u64 (accumulated with atomics; zeroed by host)
+  uint64_t* tile_counts;  // kEpiTileCount: u64[ntiles] (zeroed by host); kEpiWrite: unused
+  const uint64_t* tile_offsets;  // kEpiWrite: exclusive prefix, ntiles + 1 entries
+  uint64_t* pos;          // kEpiWrite: output positions
+  uint64_t cap;           // kEpiWrite: capacity of pos
+};
+
+// Pattern in comparison order: e[k] = off(pi(k)) | p[pi(k)] << 16.
+template <int MAXM>
+struct PatternTable {
+  uint32_t e[MAXM];
+};
+
+}  // namespace smgpu

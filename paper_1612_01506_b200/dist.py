@@ -1,0 +1,103 @@
+"""Multi-GPU partition of the text and the two exchange steps.
+
+The text t[0..N) is split into G contiguous shards.  Rank g OWNS the alignments
+[a_g, a_{g+1}) with a_g = align16(g * N / G) and HOLDS the bytes
+[a_g, min(a_{g+1} + H, N)) -- its owned bytes plus an H-byte halo (H >= m - 1
+for every pattern searched).  For a pattern of length m rank g searches the view
+t_g = held[0 : min(a_{g+1} + m - 1, N) - a_g]: its alignments are exactly the
+owned ones clipped to [0, N - m], so every occurrence is counted by exactly one
+rank and the per-rank counts add up to the global count (no overlap, no gap).
+
+Exchanges (torch.distributed over NCCL / NVLink; gloo on CPU in the tests):
+  * once per text: all_reduce(SUM) of the owned-byte histograms, so every rank
+    derives the same rarest-first order pi as a 1-GPU run (reading R14);
+  * per pattern batch: all_reduce(SUM) of the device int64 counts.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Optional
+
+ALIGN = 16
+
+
+@dataclass(frozen=True)
+class Shard:
+    rank: int
+    world: int
+    N: int          # global text length
+    own_lo: int     # first owned alignment / first held byte
+    own_hi: int     # one past the last owned alignment (= next shard's own_lo)
+    halo: int       # H: bytes held past own_hi (clipped at N)
+
+    @property
+    def held_hi(self) -> int:
+        return min(self.own_hi + self.halo, self.N)
+
+    @property
+    def held_len(self) -> int:
+        return self.held_hi - self.own_lo
+
+    @property
+    def owned_bytes(self) -> int:
+        return self.own_hi - self.own_lo
+
+    def view_len(self, m: int) -> int:
+        """Length of the local text view that counts exactly the owned alignments for length m."""
+        if m - 1 > self.halo and self.own_hi < self.N:
+            raise ValueError(f"pattern length {m} needs a halo >= {m - 1}, shard has {self.halo}")
+        return max(0, min(self.own_hi + m - 1, self.N) - self.own_lo)
+
+
+def shard_bounds(N: int, world: int) -> List[int]:
+    """a_0 = 0 <= a_1 <= ... <= a_G = N, interior cuts rounded down to 16 bytes."""
+    cuts = [0]
+    for g in range(1, world):
+        c = (g * N // world) // ALIGN * ALIGN
+        cuts.append(max(c, cuts[-1]))
+    cuts.append(N)
+    return cuts
+
+
+def make_shard(N: int, rank: int, world: int, halo: int) -> Shard:
+    if not (0 <= rank < world):
+        raise ValueError("rank out of range")
+    b = shard_bounds(N, world)
+    return Shard(rank, world, N, b[rank], b[rank + 1], halo)
+
+
+def all_shards(N: int, world: int, halo: int) -> List[Shard]:
+    return [make_shard(N, g, world, halo) for g in range(world)]
+
+
+# ----------------------------------------------------------------------------- collectives
+
+def allreduce_sum_(tensor, group=None):
+    """In-place SUM all-reduce (no-op when torch.distributed is not initialised or world == 1)."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(tensor, op=dist.ReduceOp.SUM, group=group)
+    return tensor
+
+
+def global_histogram(shard_text, shard: Shard, group=None, stream=None):
+    """Histogram of the OWNED bytes of this rank's shard, summed over ranks (device int64[256])."""
+    import paper_1612_01506_b200 as sm
+    h = sm.sm_histogram(shard_text[: shard.owned_bytes], stream=stream)
+    return allreduce_sum_(h, group)
+
+
+def count_sharded(patterns, shard_text, shard: Shard, hist, counts=None, group=None, stream=None,
+                  peel: int = 0, strategy: int = 0):
+    """Global counts of each pattern: local kernel launches + one all_reduce of int64[P]."""
+    import torch
+
+    import paper_1612_01506_b200 as sm
+    P = len(patterns)
+    if counts is None:
+        counts = torch.zeros(max(P, 1), dtype=torch.int64, device=shard_text.device)
+    for i, p in enumerate(patterns):
+        L = shard.view_len(len(p))
+        sm.sm_count_async(p, shard_text[:L], counts[i:i + 1], hist=hist, peel=peel, strategy=strategy,
+                          stream=stream)
+    return allreduce_sum_(counts, group)

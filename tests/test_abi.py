@@ -1,0 +1,78 @@
+"""CPU-side checks of the C ABI library: it loads, exports every symbol the header
+declares, and its host-only logic (order from histogram, planning, argument
+checking) behaves.  No compute call runs here (no GPU in this container)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def sm():
+    from paper_1612_01506_b200 import _build
+    _build.build()
+    import paper_1612_01506_b200 as sm
+    sm.load_library()
+    return sm
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "smgpu.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(sm_[a-z_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(sm):
+    lib = sm.load_library()
+    names = header_functions()
+    assert "sm_count" in names and "sm_report" in names and "sm_symbol_order" in names
+    for name in names:
+        assert hasattr(lib, name), name
+    assert sorted(sm.EXPORTED_SYMBOLS) == names
+
+
+def test_order_from_histogram_matches_oracle(sm):
+    rng = np.random.default_rng(0)
+    for _ in range(200):
+        m = int(rng.integers(1, 2000))
+        p = rng.integers(0, int(rng.choice([2, 4, 20, 256])), m, dtype=np.uint8).tobytes()
+        h = rng.integers(0, 1000, 256).astype(np.uint64)
+        assert sm.sm_order_from_histogram(h, p) == oracle.order(h, p).tolist()
+
+
+def test_plan_policy(sm):
+    h = np.zeros(256, dtype=np.uint64)
+    for c in b"ACGT":
+        h[c] = 1000
+    s, r = sm.sm_plan(b"ACGTACGTACGT", h)
+    assert s == sm.SM_STRATEGY_BLOCK and r == 5          # small text: alpha_eff = 512, 512*(1/4)^5 = 1/2
+    h2 = np.ones(256, dtype=np.uint64)
+    s, r = sm.sm_plan(b"hello world", h2)
+    assert s == sm.SM_STRATEGY_FILTER and r == 1
+    s, r = sm.sm_plan(b"ab", h2, strategy=sm.SM_STRATEGY_BLOCK, peel=7)
+    assert s == sm.SM_STRATEGY_BLOCK and r == 2           # r <- min(r, m)  (reading R9)
+    hz = np.zeros(256, dtype=np.uint64)
+    hz[ord("a")] = 10
+    s, r = sm.sm_plan(b"aab", hz)                         # 'b' absent -> frequency 0 -> compared first
+    assert s == sm.SM_STRATEGY_FILTER
+
+
+def test_argument_errors_without_gpu(sm):
+    lib = sm.load_library()
+    host = (ctypes.c_uint8 * 8)()
+    assert lib.sm_count(b"a", 0, ctypes.addressof(host), 8) == sm.SM_COUNT_ERROR
+    assert lib.sm_last_error() == sm.SM_EINVAL
+    assert lib.sm_count(b"a", 1, ctypes.addressof(host), 8) == sm.SM_COUNT_ERROR   # host text rejected
+    assert lib.sm_last_error() == sm.SM_EINVAL
+    assert lib.sm_count(b"a", 1, None, 8) == sm.SM_COUNT_ERROR
+    lib.sm_clear_error()
+    assert lib.sm_last_error() == sm.SM_OK
+    assert lib.sm_status_string(2) == b"SM_ETRUNC"
+    with pytest.raises(sm.SmError):
+        sm.sm_plan(b"ab", np.ones(256), order=[1, 1])

@@ -1,0 +1,258 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle, element by element.
+
+Integer work throughout, so the bar is bit-exact: counts, positions, histograms
+and orders must equal the oracle's.  Strategy, peeling factor r, comparison
+order pi, tile size and the text's byte offset are free parameters that must
+never change a result ("Clearly ... iff the k-bit of found is set":
+AND is commutative, so any order/peeling gives Alg. 1's answer).
+"""
+import ctypes
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def sm():
+    import paper_1612_01506_b200 as sm
+    sm.load_library()
+    return sm
+
+
+def dev(a: np.ndarray, offset: int = 0):
+    """Device copy of host bytes `a`, placed at byte `offset` of a fresh allocation (unaligned views)."""
+    buf = torch.empty(a.size + offset + 16, dtype=torch.uint8, device="cuda")
+    buf.fill_(0xEE)
+    if a.size:
+        buf[offset: offset + a.size].copy_(torch.from_numpy(np.ascontiguousarray(a)))
+    return buf[offset: offset + a.size]
+
+
+def count_async(sm, p, t, **kw):
+    d = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    sm.sm_count_async(p, t, d, **kw)
+    return int(d.item())
+
+
+def report_async(sm, p, t, cap, **kw):
+    d = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    pos = torch.full((max(cap, 1),), -7, dtype=torch.int64, device="cuda")
+    sm.sm_report_async(p, t, pos[:cap] if cap else None, d, **kw)
+    total = int(d.item())
+    return pos[: min(cap, total)].cpu().numpy(), total
+
+
+# ------------------------------------------------------------------------------------------- Fig. 1
+def test_fig1(sm):
+    import json, os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "fig1.json")))
+    t = dev(np.frombuffer(g["t"].encode(), dtype=np.uint8))
+    p = g["p"].encode()
+    assert sm.sm_count(p, t) == g["count"]
+    pos, total = sm.sm_report(p, t)
+    assert total == g["count"] and pos.cpu().tolist() == g["positions_0based"]
+    assert sm.sm_symbol_order(t, p) == g["order_0based"]
+    for strat in (1, 2):
+        for r in (1, 2, 3, 4):
+            assert count_async(sm, p, t, strategy=strat, peel=r) == 1
+
+
+# ------------------------------------------------------------------------------------------- closed forms
+@pytest.mark.parametrize("n", [1, 15, 16, 17, 4096, 65537, 300000])
+def test_periodic_closed_form(sm, n):
+    t = dev(np.full(n, 0x61, dtype=np.uint8), offset=n % 7)
+    for m in (1, 2, 17, 1000):
+        for strat in (0, 1, 2):
+            want = max(n - m + 1, 0)
+            assert count_async(sm, b"a" * m, t, strategy=strat) == want, (n, m, strat)
+            assert count_async(sm, b"a" * (m - 1) + b"b", t, strategy=strat) == 0
+
+
+def test_edge_cases(sm):
+    t = dev(np.frombuffer(b"abcabcab", dtype=np.uint8))
+    assert sm.sm_count(b"abcabcabc", t) == 0          # m > n
+    assert sm.sm_count(b"abcabcab", t) == 1           # p = t
+    empty = torch.empty(0, dtype=torch.uint8, device="cuda")
+    assert sm.sm_count(b"a", empty) == 0              # n = 0
+    pos, total = sm.sm_report(b"ab", t)
+    assert total == 3 and pos.cpu().tolist() == [0, 3, 6]
+    assert sm.sm_count(b"\x00", dev(np.zeros(33, dtype=np.uint8))) == 33   # NUL is a symbol
+
+
+def test_errors(sm):
+    t = dev(np.frombuffer(b"hello", dtype=np.uint8))
+    with pytest.raises(sm.SmError) as e:
+        sm.sm_count(b"", t)
+    assert e.value.status == sm.SM_EINVAL
+    with pytest.raises(sm.SmError):
+        sm.sm_count(b"x" * (sm.SM_MAX_PATTERN + 1), dev(np.zeros(10000, dtype=np.uint8)))
+    lib = sm.load_library()
+    host = (ctypes.c_uint8 * 64)()
+    r = lib.sm_count(b"ab", 2, ctypes.addressof(host), 64)   # host text: rejected, no CPU fallback
+    assert r == sm.SM_COUNT_ERROR and lib.sm_last_error() == sm.SM_EINVAL
+    with pytest.raises(sm.SmError):
+        count_async(sm, b"ab", t, order=[0, 0])
+
+
+# ------------------------------------------------------------------------------------------- histogram / order
+@pytest.mark.parametrize("n,off", [(0, 0), (1, 3), (15, 1), (16, 0), (17, 15), (4099, 5), (1 << 20, 9), (3_000_001, 0)])
+def test_histogram(sm, n, off):
+    rng = np.random.default_rng(n + off)
+    a = rng.integers(0, 256, n, dtype=np.uint8) if n % 2 else (rng.zipf(1.3, n) % 256).astype(np.uint8)
+    t = dev(a, off)
+    got = sm.sm_histogram(t).cpu().numpy().astype(np.uint64)
+    assert np.array_equal(got, oracle.hist(a))
+
+
+def test_symbol_order_matches_oracle(sm):
+    spec = synth.text_spec("c2", n=1 << 18)
+    a = spec.host()
+    t = dev(a)
+    h = oracle.hist(a)
+    rng = np.random.default_rng(7)
+    for m in (1, 2, 5, 64, 333, 1024, 4096):
+        s = int(rng.integers(0, a.size - m))
+        p = a[s:s + m].tobytes()
+        want = oracle.order(h, p).tolist()
+        assert sm.sm_symbol_order(t, p) == want
+        assert sm.sm_order_from_histogram(h, p) == want
+
+
+# ------------------------------------------------------------------------------------------- differential
+def _case(rng):
+    sigma = int(rng.choice([1, 2, 4, 20, 96, 256]))
+    n = int(rng.choice([0, 1, 7, 16, 100, 1000, 4095, 4096, 4097, 20000, 65536, 70001]))
+    n = max(0, n + int(rng.integers(-3, 4)))
+    m = int(rng.choice([1, 2, 3, 4, 5, 8, 13, 16, 17, 31, 32, 64, 100, 255, 1024, 4096]))
+    a = rng.integers(0, sigma, n, dtype=np.uint8) + int(rng.integers(0, 256 - sigma + 1))
+    a = a.astype(np.uint8)
+    if n >= m and rng.random() < 0.75:
+        s = int(rng.integers(0, n - m + 1))
+        p = a[s:s + m].tobytes()
+    else:
+        p = (rng.integers(0, sigma, m) + (a[0] if n else 0)).astype(np.uint8).tobytes()
+    return a, p
+
+
+def test_random_differential_count(sm):
+    rng = np.random.default_rng(1234)
+    for trial in range(600):
+        a, p = _case(rng)
+        m = len(p)
+        off = int(rng.integers(0, 16))
+        t = dev(a, off)
+        want = oracle.naive_count(p, a)
+        h = oracle.hist(a)
+        strat = int(rng.integers(0, 3))
+        peel = int(rng.integers(0, m + 2))
+        order = rng.permutation(m).tolist() if rng.random() < 0.4 else None
+        got = count_async(sm, p, t, hist=h, order=order, peel=peel, strategy=strat)
+        assert got == want, dict(trial=trial, n=a.size, m=m, off=off, strat=strat, peel=peel)
+
+
+def test_random_differential_report(sm):
+    rng = np.random.default_rng(99)
+    for trial in range(250):
+        a, p = _case(rng)
+        off = int(rng.integers(0, 16))
+        t = dev(a, off)
+        want = oracle.naive_report(p, a)
+        strat = int(rng.integers(0, 3))
+        order = rng.permutation(len(p)).tolist() if rng.random() < 0.3 else None
+        pos, total = report_async(sm, p, t, cap=want.size + 3, hist=oracle.hist(a), order=order, strategy=strat)
+        assert total == want.size
+        assert pos.astype(np.uint64).tolist() == want.tolist(), dict(trial=trial, n=a.size, m=len(p), strat=strat)
+
+
+def test_report_truncation(sm):
+    a = np.frombuffer(b"ab" * 5000, dtype=np.uint8)
+    t = dev(a)
+    want = oracle.naive_report(b"ab", a)
+    for strat in (1, 2):
+        pos, total = report_async(sm, b"ab", t, cap=100, strategy=strat)
+        assert total == 5000 and pos.tolist() == want[:100].tolist()
+    pos, total = sm.sm_report(b"ab", t, cap=7)
+    assert total == 5000 and pos.cpu().tolist() == want[:7].tolist()
+    lib = sm.load_library()
+    assert lib.sm_last_error() == sm.SM_ETRUNC
+
+
+def test_dense_report_every_alignment(sm):
+    n = 300_003
+    t = dev(np.full(n, 7, dtype=np.uint8), 3)
+    for m, strat in ((1, 2), (3, 2), (3, 1)):
+        pos, total = report_async(sm, bytes([7]) * m, t, cap=n, strategy=strat)
+        assert total == n - m + 1
+        assert np.array_equal(pos, np.arange(n - m + 1))
+
+
+# ------------------------------------------------------------------------------------------- seams
+def test_tile_seams(sm):
+    """Occurrences planted across every tile / chunk / warp boundary, for both tile sizes."""
+    rng = np.random.default_rng(5)
+    for n in (64 * 4096 - 5, 600 * 16384 + 11):
+        a = rng.integers(0, 200, n, dtype=np.uint8)
+        for m in (2, 16, 33, 700):
+            p = (rng.integers(200, 256, m)).astype(np.uint8)
+            b = a.copy()
+            starts = []
+            for T in (4096, 16384):
+                for k in range(1, n // T):
+                    for d in (-m + 1, -m // 2, -1, 0, 1):
+                        s = k * T + d
+                        if 0 <= s <= n - m:
+                            starts.append(s)
+            starts = sorted(set(starts))[:: max(1, len(starts) // 400)]
+            kept = []
+            for s in starts:          # keep planted copies non-overlapping
+                if not kept or s >= kept[-1] + m:
+                    b[s:s + m] = p
+                    kept.append(s)
+            for off in (0, 5):
+                t = dev(b, off)
+                want = oracle.naive_count(p.tobytes(), b)
+                assert want >= len(kept)
+                for strat in (1, 2):
+                    assert count_async(sm, p.tobytes(), t, strategy=strat) == want, (n, m, off, strat)
+
+
+def test_boundary_residues(sm):
+    """n - m + 1 at every residue mod 16 and around tile sizes; matches at the very end."""
+    rng = np.random.default_rng(11)
+    for base in (32, 4096, 16384 * 300):
+        for dn in range(0, 16):
+            n = base + dn
+            a = rng.integers(0, 4, n, dtype=np.uint8)
+            for m in (1, 5, 16):
+                p = a[n - m:].tobytes()      # occurrence ending at t[n-1]
+                want = oracle.naive_count(p, a)
+                t = dev(a, dn % 3)
+                for strat in (1, 2):
+                    assert count_async(sm, p, t, strategy=strat) == want
+
+
+# ------------------------------------------------------------------------------------------- virtual shards
+def test_virtual_shards_sum(sm):
+    from paper_1612_01506_b200 import dist
+    spec = synth.text_spec("c5", n=(1 << 22) + 13)
+    a = spec.host()
+    t = dev(a)
+    H = 63
+    for m in (8, 16, 64):
+        pats = [a[s:s + m].tobytes() for s in
+                [x for cut in dist.shard_bounds(a.size, 8)[1:-1] for x in (cut - 1, cut - m // 2, cut - m + 1, cut)]]
+        for p in pats[:12]:
+            want = oracle.naive_count(p, a)
+            for G in (1, 2, 3, 8):
+                tot = 0
+                for sh in dist.all_shards(a.size, G, H):
+                    view = t[sh.own_lo: sh.own_lo + sh.view_len(m)]
+                    tot += count_async(sm, p, view)
+                assert tot == want, (m, G)
