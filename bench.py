@@ -235,18 +235,17 @@ def run_native(args):
     views = [text[: shard.view_len(p.m)] for p in pats]
     counts = torch.zeros(P, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream()
-    ev_pairs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(P)]
 
-    def step(record=False):
+    def step(ev=None):
         h = smd.global_histogram(text, shard)             # A1 (+ all_reduce)
         hh = h.cpu().numpy().astype(np.uint64)           # 2 KiB D2H for the host-side order (A2)
-        for i in range(P):
-            if record:
-                ev_pairs[i][0].record(stream)
+        if ev is not None:
+            ev[0].record(stream)
+        for i in range(P):                               # A2 (host) + A3..A7 (one launch each)
             sm.sm_count_async(pdata[i], views[i], counts[i:i + 1], hist=hh, peel=args.peel,
                               strategy=args.strategy)
-            if record:
-                ev_pairs[i][1].record(stream)
+        if ev is not None:
+            ev[1].record(stream)
         smd.allreduce_sum_(counts)
         return hh
 
@@ -263,19 +262,17 @@ def run_native(args):
     clk = ClockSampler(local)
     clk.start()
     launches0 = sm.sm_launch_count()
-    kern_ms = np.zeros(P)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     start.record(stream)
     for s in range(args.steps):
-        step(record=True)
-        if s == args.steps - 1:
-            end.record(stream)
-        torch.cuda.synchronize()
-        kern_ms += np.array([a.elapsed_time(b) for a, b in ev_pairs])
+        step(evs[s])
+    end.record(stream)
     barrier()
     launches = sm.sm_launch_count() - launches0
     total_ms = start.elapsed_time(end)
+    search_ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps   # the P search launches of a step
     clocks = clk.stop()
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -285,18 +282,29 @@ def run_native(args):
     bytes_per_step = spec.n * P
     value = bytes_per_step / (ms_per_step * 1e-3) / 1e9
 
-    # per-kernel roofline (this rank's launches, averaged)
-    kern_ms /= args.steps
+    # roofline of the dominant kernel (this rank): algorithmic bytes (n of each launch's
+    # view) / average launch duration, from the events bracketing the step's launches
     local_bytes = np.array([v.numel() for v in views], dtype=np.float64)
     peak, peak_kind, pk = peaks()
-    achieved = float(local_bytes.sum() / (kern_ms.sum() * 1e-3) / 1e9)
+    achieved = float(local_bytes.sum() / (search_ms * 1e-3) / 1e9)
     lens = sorted({p.m for p in pats})
+
+    # per-length breakdown (diagnostic pass after the timed region; same launches)
     per_m = {}
     for m in lens:
         idx = [i for i, p in enumerate(pats) if p.m == m]
-        gbs = float(local_bytes[idx].sum() / (kern_ms[idx].sum() * 1e-3) / 1e9)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in idx:
+            sm.sm_count_async(pdata[i], views[i], counts[i:i + 1], hist=hh)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        gbs = float(local_bytes[idx].sum() / (ms * 1e-3) / 1e9)
         per_m[str(m)] = {"GBps": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4),
-                         "us_per_launch": round(float(kern_ms[idx].mean() * 1e3), 2)}
+                         "us_per_launch": round(ms * 1e3 / len(idx), 2)}
+    step()  # restore counts of the full step
+    torch.cuda.synchronize()
     counts_host = counts.cpu().numpy()
 
     # ---------------- end-to-end through the public API (host text in pinned memory)
@@ -395,7 +403,7 @@ def run_native(args):
         "gpu_launches": int(launches),
         "roofline": {
             "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": None,
+            "frac": round(achieved / peak, 4), "traffic": None, "avg_launch_us": round(search_ms * 1e3 / P, 2),
             "kernel": "search_kernel (count)", "peak_kind": peak_kind,
             "algorithmic_bytes_per_launch": "n (text bytes of the launch's view)",
         },

@@ -137,7 +137,10 @@ def _u64_host(a) -> Optional[np.ndarray]:
         return None
     if hasattr(a, "detach"):
         a = a.detach().cpu().numpy()
-    return np.ascontiguousarray(np.asarray(a).astype(np.uint64))
+    a = np.asarray(a)
+    if a.dtype != np.uint64:
+        a = a.astype(np.uint64)
+    return np.ascontiguousarray(a)
 
 
 def _u32_host(a) -> Optional[np.ndarray]:

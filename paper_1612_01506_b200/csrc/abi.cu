@@ -2,6 +2,7 @@
 // peeling factor r, strategy, tiling) and launch orchestration.  Host code only;
 // every step of the path on the text runs in the kernels of this library.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -77,12 +78,29 @@ sm_status check_pattern_text(const uint8_t* p, size_t m, const uint8_t* t, size_
   return SM_OK;
 }
 
-// stable rarest-first order (ties by position, R11)
+// stable rarest-first order (ties by position, R11).  A stable
+// counting sort: the distinct key values hist[c] of the symbols in p are ranked
+// (at most 256 of them), then positions are bucketed by rank in ascending order.
+// O(m + 256 log 256); equals std::stable_sort by hist[p[j]].
 void order_from_hist(const uint64_t* hist, const uint8_t* p, size_t m, uint32_t* order) {
-  std::vector<uint32_t> idx(m);
-  for (size_t j = 0; j < m; ++j) idx[j] = (uint32_t)j;
-  std::stable_sort(idx.begin(), idx.end(), [&](uint32_t a, uint32_t b) { return hist[p[a]] < hist[p[b]]; });
-  std::memcpy(order, idx.data(), m * sizeof(uint32_t));
+  bool present[256] = {false};
+  for (size_t j = 0; j < m; ++j) present[p[j]] = true;
+  uint8_t syms[256];
+  int ns = 0;
+  for (int c = 0; c < 256; ++c)
+    if (present[c]) syms[ns++] = (uint8_t)c;
+  std::sort(syms, syms + ns, [&](uint8_t x, uint8_t y) { return hist[x] < hist[y]; });
+  uint32_t rank[256];
+  int nr = 0;
+  for (int i = 0; i < ns; ++i) {
+    if (i > 0 && hist[syms[i]] != hist[syms[i - 1]]) ++nr;
+    rank[syms[i]] = (uint32_t)nr;
+  }
+  ++nr;
+  uint32_t start[257] = {0};
+  for (size_t j = 0; j < m; ++j) ++start[rank[p[j]] + 1];
+  for (int r = 0; r < nr; ++r) start[r + 1] += start[r];
+  for (size_t j = 0; j < m; ++j) order[start[rank[p[j]]]++] = (uint32_t)j;
 }
 
 bool valid_permutation(const uint32_t* order, size_t m) {
@@ -94,7 +112,29 @@ bool valid_permutation(const uint32_t* order, size_t m) {
   return true;
 }
 
-constexpr double kFilterMaxF = 0.10;  // FILTER when the rarest pattern symbol has freq <= this
+// Performance knobs (never change results).  Defaults tuned on B200; SMGPU_* env
+// variables override them once per process for tuning sweeps.
+struct Tunables {
+  uint32_t tile = 32768;        // text bytes per tile for large texts (4096 * CPL)
+  int ctas_per_sm = 2;          // persistent CTAs per SM
+  uint32_t max_stages = 8;      // ring depth cap per CTA
+  double filter_max_f = 0.10;   // AUTO: FILTER when the rarest pattern symbol has frequency <= this
+};
+
+const Tunables& tunables() {
+  static const Tunables t = [] {
+    Tunables x;
+    if (const char* e = std::getenv("SMGPU_TILE")) x.tile = (uint32_t)std::atoi(e);
+    if (const char* e = std::getenv("SMGPU_CTAS_PER_SM")) x.ctas_per_sm = std::atoi(e);
+    if (const char* e = std::getenv("SMGPU_STAGES")) x.max_stages = (uint32_t)std::atoi(e);
+    if (const char* e = std::getenv("SMGPU_FILTER_MAX_F")) x.filter_max_f = std::atof(e);
+    if (x.tile != 4096 && x.tile != 8192 && x.tile != 16384 && x.tile != 32768) x.tile = 32768;
+    if (x.ctas_per_sm < 1 || x.ctas_per_sm > 3) x.ctas_per_sm = 2;
+    if (x.max_stages < 2 || x.max_stages > (uint32_t)kMaxStages) x.max_stages = kMaxStages;
+    return x;
+  }();
+  return t;
+}
 
 struct Plan {
   int strategy = kFilter;
@@ -106,12 +146,10 @@ struct Plan {
 
 void choose_tiling(uint64_t n, Plan& pl) {
   const uint64_t sms = (uint64_t)num_sms();
-  pl.tile = 16384;
-  pl.cpl = 4;
-  if ((n + pl.tile - 1) / pl.tile < 2 * sms) {
-    pl.tile = 4096;
-    pl.cpl = 1;
-  }
+  pl.tile = tunables().tile;
+  // small texts: shrink the tile until every CTA slot gets work
+  while (pl.tile > 4096 && (n + pl.tile - 1) / pl.tile < sms * (uint64_t)tunables().ctas_per_sm) pl.tile /= 2;
+  pl.cpl = (int)(pl.tile / (16u * kLanesPerTilePass));
 }
 
 sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist, const uint32_t* order,
@@ -128,7 +166,7 @@ sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist
   double total = 0;
   for (int c = 0; c < 256; ++c) total += (double)hist[c];
   auto freq = [&](size_t k) { return total > 0 ? (double)hist[p[pl.order[k]]] / total : 0.0; };
-  if (strategy == SM_STRATEGY_AUTO) strategy = freq(0) <= kFilterMaxF ? kFilter : kBlock;
+  if (strategy == SM_STRATEGY_AUTO) strategy = freq(0) <= tunables().filter_max_f ? kFilter : kBlock;
   pl.strategy = strategy;
   if (peel == 0) {
     // smallest r with alpha_eff * prod_{k<r} f(pi(k)) <= 1/2 (PAPER.md:176-178 reasoning at alpha_eff)
@@ -176,7 +214,13 @@ void make_args(const Plan& pl, const uint8_t* p, size_t m, const uint8_t* t, siz
     a.a1 = a1;
     a.bc1 = (uint32_t)p[a1] * 0x01010101u;
     a.pre = (a1 + 15) & ~15u;
-    const uint32_t post = ((uint32_t)(m - 1 - a1) + 15) & ~15u;
+    if (m >= 2) {
+      const uint32_t a2 = pl.order[1];
+      a.s2 = a.pre + a2 - a1;
+      a.bc2 = (uint32_t)p[a2] * 0x01010101u;
+    }
+    // + 16: the pi(2) window of the last chunk reads up to 32 bytes past its base
+    const uint32_t post = (((uint32_t)(m - 1 - a1) + 15) & ~15u) + 16;
     a.stage_len = (uint32_t)T + a.pre + post;
     a.k_begin = (a.delta + a1) / T;
     const uint64_t k_end = (a.delta + a.A - 1 + a1) / T + 1;
@@ -188,15 +232,28 @@ void make_args(const Plan& pl, const uint8_t* p, size_t m, const uint8_t* t, siz
     a.k_begin = 0;
     a.ntiles = (a.delta + a.A - 1) / T + 1;
   }
+  {  // edge tiles: only these need range masks (tile ti covers alignments x_base + [0, T))
+    const uint64_t shift = pl.strategy == kFilter ? a.a1 : 0;
+    const uint64_t first_full = (a.delta + shift + T - 1) / T;  // smallest k with k*T - shift >= delta
+    a.edge_lo = first_full > a.k_begin ? first_full - a.k_begin : 0;
+    const uint64_t kh = (a.delta + a.A + shift) / T;             // smallest k with (k+1)*T - shift > delta + A
+    a.edge_hi = kh > a.k_begin ? kh - a.k_begin : 0;
+  }
   a.stage_stride = (a.stage_len + 127) & ~127u;
-  a.tbl_off = 2 * kMaxStages * 8 + 2 * 4 * kConsumerWarps * 4;  // barriers + write-epilogue scratch
-  a.ring_off = (a.tbl_off + 4 * (uint32_t)m + 127) & ~127u;
-  const uint32_t budget = 227 * 1024;
-  uint32_t stages = (budget - a.ring_off) / a.stage_stride;
-  a.stages = std::min<uint32_t>(stages, kMaxStages);
+  a.ring_off = (kTblOff + 4 * (uint32_t)m + 127) & ~127u;
+  // shared memory per SM: 228 KiB, 1 KiB reserved per resident CTA
+  int ctas = tunables().ctas_per_sm;
+  uint32_t stages = 0;
+  for (; ctas >= 1; --ctas) {
+    const uint32_t budget = std::min<uint32_t>(227 * 1024, 233472 / ctas - 1024);
+    stages = budget > a.ring_off ? (budget - a.ring_off) / a.stage_stride : 0;
+    if (stages >= 2) break;
+  }
+  if (ctas < 1) ctas = 1;
+  a.stages = std::min<uint32_t>(stages, tunables().max_stages);
   smem = (size_t)a.ring_off + (size_t)a.stages * a.stage_stride;
   const uint64_t sms = (uint64_t)num_sms();
-  grid = (int)std::min<uint64_t>(a.ntiles, sms);
+  grid = (int)std::min<uint64_t>(a.ntiles, sms * (uint64_t)ctas);
   if (grid < 1) grid = 1;
 }
 

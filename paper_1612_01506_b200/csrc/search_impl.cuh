@@ -1,0 +1,439 @@
+// search_impl.cuh -- the hot path: exact occurrence counting / reporting of a
+// pattern in a device-resident byte text, pattern symbols compared rarest-first
+// with peeled first comparisons (Algs. 3-4), B200-native.
+//
+// Persistent CTAs (several per SM): warp 8 is the TMA producer, warps 0..7 compare.
+//   * A3 staging (PAPER.md:101-106 loads 16/32 unaligned bytes; here): tiles of
+//     T text bytes plus the pattern's halo are copied HBM -> shared memory with
+//     1-D TMA bulk copies (cp.async.bulk, 16-B granules, L2 evict-first) into a
+//     ring of mbarrier-guarded stages.  Ragged 16-B ends of the text are loaded
+//     byte-wise by the producer so nothing outside t[0..n) is read.
+//   * The SIMDcompare primitive becomes a packed-byte compare:
+//     each lane owns chunks of 16 consecutive alignments held as 4 x u32 words
+//     with one flag bit (0x80) per alignment.
+//   * FILTER strategy: the first comparison pi(1) -- the rarest symbol, where the
+//     paper's frequency order pays most -- runs over the chunk
+//     with aligned 16-B shared loads; each surviving alignment continues with
+//     pi(2..m) and early exit (Alg. 3's inner loop at alpha = 1).
+//   * BLOCK strategy: Alg. 4: r peeled comparisons without a
+//     test, then the pi-ordered loop with a warp-uniform exit
+//     test (__any_sync) over all alignments the warp holds.
+//   * A6: popcount -> warp reduce -> one u64 atomic per warp.
+//   * A8: reporting writes ascending positions from a per-tile exclusive prefix.
+#pragma once
+#include "device_util.cuh"
+#include "launch.h"
+#include "search.cuh"
+
+namespace smgpu {
+
+namespace {
+
+__device__ __forceinline__ int64_t imax(int64_t a, int64_t b) { return a > b ? a : b; }
+__device__ __forceinline__ int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
+
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// TMA producer (one thread)
+// ---------------------------------------------------------------------------
+template <int EPI>
+__device__ void produce(const SearchArgs& a, uint8_t* ring, uint64_t* full, uint64_t* empty) {
+  const uint64_t pol = l2_policy_evict_first();
+  const int64_t tlo = (int64_t)a.delta, thi = (int64_t)(a.delta + a.n);
+  uint32_t s = 0, ph = 0;  // stage and its use parity
+  bool wrapped = false;
+  for (uint64_t ti = blockIdx.x; ti < a.ntiles; ti += gridDim.x) {
+    if (EPI == kEpiWrite && a.tile_offsets[ti + 1] == a.tile_offsets[ti]) continue;
+    if (wrapped) mbar_wait_sleep(&empty[s], ph ^ 1u);  // consumers released this stage's previous use
+    uint8_t* buf = ring + (size_t)s * a.stage_stride;
+    const int64_t lo = (int64_t)((a.k_begin + ti) * a.tile) - (int64_t)a.pre;
+    const int64_t hi = lo + (int64_t)a.stage_len;
+    const int64_t vlo = imax(lo, tlo), vhi = imin(hi, thi);
+    uint32_t tx = 0;
+    int64_t alo = 0;
+    if (vlo < vhi) {
+      alo = (vlo + 15) & ~(int64_t)15;
+      const int64_t ahi = vhi & ~(int64_t)15;
+      bool ragged = false;
+      if (alo < ahi) {
+        for (int64_t o = vlo; o < alo; ++o) { buf[o - lo] = ldg_u8_nc(a.base + o); ragged = true; }
+        for (int64_t o = ahi; o < vhi; ++o) { buf[o - lo] = ldg_u8_nc(a.base + o); ragged = true; }
+        tx = (uint32_t)(ahi - alo);
+      } else {
+        for (int64_t o = vlo; o < vhi; ++o) { buf[o - lo] = ldg_u8_nc(a.base + o); ragged = true; }
+      }
+      if (ragged) fence_proxy_async_smem();
+    }
+    mbar_arrive_expect_tx(&full[s], tx);
+    if (tx) tma_load_1d(buf + (alo - lo), a.base + alo, tx, &full[s], pol);
+    if (++s == a.stages) {
+      s = 0;
+      ph ^= 1u;
+      wrapped = true;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Packed-byte helpers for one lane-chunk of 16 alignments (4 x u32 flag words,
+// 0x80 per surviving alignment: the sm_100a form of the paper's `found`).
+// ---------------------------------------------------------------------------
+struct Found4 {
+  uint32_t f0, f1, f2, f3;
+};
+
+// 16 bytes starting at smem address base16 + sel (base16 16-B aligned, sel in 0..15
+// warp-uniform): two conflict-free LDS.128 + funnel shifts.  This is SIMDcompare's
+// unaligned load (PAPER.md:101 _mm_loadu_si128) on shared memory.
+__device__ __forceinline__ uint4 load_window16(const uint8_t* base16, uint32_t sel) {
+  const uint4 lo = lds128(base16);
+  const uint4 hi = lds128(base16 + 16);
+  const uint32_t sh = (sel & 3u) * 8u;
+  uint4 w;
+  switch ((sel >> 2) & 3u) {
+    case 0:
+      w.x = byte_window(lo.x, lo.y, sh); w.y = byte_window(lo.y, lo.z, sh);
+      w.z = byte_window(lo.z, lo.w, sh); w.w = byte_window(lo.w, hi.x, sh);
+      break;
+    case 1:
+      w.x = byte_window(lo.y, lo.z, sh); w.y = byte_window(lo.z, lo.w, sh);
+      w.z = byte_window(lo.w, hi.x, sh); w.w = byte_window(hi.x, hi.y, sh);
+      break;
+    case 2:
+      w.x = byte_window(lo.z, lo.w, sh); w.y = byte_window(lo.w, hi.x, sh);
+      w.z = byte_window(hi.x, hi.y, sh); w.w = byte_window(hi.y, hi.z, sh);
+      break;
+    default:
+      w.x = byte_window(lo.w, hi.x, sh); w.y = byte_window(hi.x, hi.y, sh);
+      w.z = byte_window(hi.y, hi.z, sh); w.w = byte_window(hi.z, hi.w, sh);
+      break;
+  }
+  return w;
+}
+
+// found &= SIMDcompare(...) for the 16 alignments whose compared bytes are `w`
+__device__ __forceinline__ void found_and_eq(Found4& F, const uint4 w, uint32_t bc) {
+  F.f0 &= eq_flags_raw(w.x, bc);
+  F.f1 &= eq_flags_raw(w.y, bc);
+  F.f2 &= eq_flags_raw(w.z, bc);
+  F.f3 &= eq_flags_raw(w.w, bc);
+}
+
+__device__ __forceinline__ Found4 found_all() { return Found4{0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u}; }
+
+__device__ __forceinline__ Found4 found_from_mask16(uint32_t vmask) {
+  return Found4{nibble_to_flags(vmask & 0xFu), nibble_to_flags((vmask >> 4) & 0xFu),
+                nibble_to_flags((vmask >> 8) & 0xFu), nibble_to_flags((vmask >> 12) & 0xFu)};
+}
+
+__device__ __forceinline__ uint32_t found_mask16(const Found4& F) {
+  return flags_to_nibble(F.f0) | (flags_to_nibble(F.f1) << 4) | (flags_to_nibble(F.f2) << 8) |
+         (flags_to_nibble(F.f3) << 12);
+}
+
+__device__ __forceinline__ uint32_t found_any(const Found4& F) { return (F.f0 | F.f1 | F.f2 | F.f3) & 0x80808080u; }
+
+// bits b in [0,16) with lo <= u0 + b < hi (tile-relative 32-bit coordinates)
+__device__ __forceinline__ uint32_t range_mask16_rel(int32_t u0, int32_t lo, int32_t hi) {
+  int32_t l = min(max(lo - u0, 0), 16), h = min(max(hi - u0, 0), 16);
+  if (h <= l) return 0u;
+  return ((1u << h) - 1u) & ~((1u << l) - 1u);
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, v, d);
+    if (lane >= d) v += u;
+  }
+  return v;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t r;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+  return r;
+}
+
+// FILTER phase A: does any of the 16 pi(1)-bytes of a chunk equal p[pi(1)]?
+// (borrow-based zero-byte test: exact as a whole-chunk predicate)
+__device__ __forceinline__ bool chunk_hit(const uint4 v, uint32_t bc) {
+  return ((any_eq_term(v.x, bc) | any_eq_term(v.y, bc) | any_eq_term(v.z, bc) | any_eq_term(v.w, bc)) &
+          0x80808080u) != 0;
+}
+
+// 0x80-per-byte flag words -> one word, bit (8k + 7 - i) <-> alignment 4i + k
+__device__ __forceinline__ uint32_t compress_found(const Found4& F) {
+  return (F.f0 & 0x80808080u) | ((F.f1 & 0x80808080u) >> 1) | ((F.f2 & 0x80808080u) >> 2) |
+         ((F.f3 & 0x80808080u) >> 3);
+}
+__device__ __forceinline__ uint32_t gbit_to_alignment(uint32_t p) { return 4u * (7u - (p & 7u)) + (p >> 3); }
+
+__device__ __forceinline__ uint32_t g_to_mask16(uint32_t g) {
+  uint32_t m16 = 0;
+  while (g) {
+    const uint32_t p = __ffs(g) - 1;
+    g &= g - 1;
+    m16 |= 1u << gbit_to_alignment(p);
+  }
+  return m16;
+}
+
+// FILTER phase B for one queued chunk c: Alg. 4's peeled part with r = 2 on its
+// 16 alignments -- exact packed-byte compares of pi(1) and pi(2) without a test
+// in between.  Returns the compressed found word (bit
+// (8k + 7 - i) <-> tile-relative alignment u = 16c + 4i + k) of the survivors.
+__device__ __forceinline__ uint32_t filter_entry(const SearchArgs& a, const uint8_t* buf, const uint32_t* tbl,
+                                                 uint32_t c, bool edge, int32_t rlo, int32_t rhi) {
+  Found4 F = edge ? found_from_mask16(range_mask16_rel((int32_t)(16u * c), rlo, rhi)) : found_all();
+  found_and_eq(F, lds128(buf + a.pre + 16u * c), a.bc1);                                       // pi(1)
+  if (a.m >= 2) found_and_eq(F, load_window16(buf + 16u * c + (a.s2 & ~15u), a.s2), a.bc2);  // pi(2)
+  return compress_found(F);
+}
+
+// pi(3..m) for the survivors of pi(1), pi(2) held by the lanes of a warp (g = 0 on
+// lanes without).  Survivors are rare, so the whole warp verifies one at a time:
+// each step compares 32 consecutive positions of the order pi in parallel and
+// exits at the first step with a mismatch (Alg. 3's early exit with 32 pattern
+// positions per step; any order gives the same result).
+__device__ __forceinline__ uint32_t verify_survivors(const SearchArgs& a, const uint8_t* buf, const uint32_t* tbl,
+                                                     uint32_t c, uint32_t g, int lane) {
+  uint32_t todo = __ballot_sync(0xFFFFFFFFu, g != 0);
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    todo &= todo - 1;
+    uint32_t gs = __shfl_sync(0xFFFFFFFFu, g, src);
+    const uint32_t cs = __shfl_sync(0xFFFFFFFFu, c, src);
+    uint32_t keep = gs;
+    const uint8_t* xb = buf + a.pre + 16u * cs - a.a1;  // smem address of alignment u = 16 cs
+    while (gs) {
+      const uint32_t p = __ffs(gs) - 1;
+      gs &= gs - 1;
+      const uint8_t* xp = xb + gbit_to_alignment(p);
+      for (uint32_t q0 = 2; q0 < a.m; q0 += 32) {
+        const uint32_t q = q0 + lane;
+        bool mis = false;
+        if (q < a.m) {
+          const uint32_t e = tbl[q];
+          mis = xp[e & 0xFFFFu] != (e >> 16);
+        }
+        if (__any_sync(0xFFFFFFFFu, mis)) {
+          keep &= ~(1u << p);
+          break;
+        }
+      }
+    }
+    if (lane == src) g = keep;
+  }
+  return g;
+}
+
+// Positions of one warp's chunk stream, written in ascending order (input: compressed found word).
+struct WriteSink {
+  uint64_t run;    // next output index of this warp
+  int64_t pbase;   // 0-based position of u = 0
+  uint64_t* pos;
+  uint64_t cap;
+  __device__ __forceinline__ void operator()(uint32_t c, uint32_t m16, int lane) {
+    m16 = g_to_mask16(m16);
+    const uint32_t pc = __popc(m16);
+    const uint32_t incl = warp_incl_scan(pc, lane);
+    uint64_t idx = run + incl - pc;
+    while (m16) {
+      const uint32_t b = __ffs(m16) - 1;
+      m16 &= m16 - 1;
+      if (idx < cap) pos[idx] = (uint64_t)(pbase + 16 * (int64_t)c + b);
+      ++idx;
+    }
+    run += __shfl_sync(0xFFFFFFFFu, incl, 31);
+  }
+};
+
+struct CountSink {
+  uint32_t n = 0;
+  __device__ __forceinline__ void operator()(uint32_t, uint32_t m16, int) { n += __popc(m16); }
+};
+
+// One warp's share of a FILTER tile, in groups of kGroup chunk-rows: phase A
+// ballot-compacts the chunks whose pi(1)-bytes contain p[pi(1)] into the warp's
+// queue (ascending chunk order); phase B drains it 32 entries at a time, one
+// chunk per lane, all lanes busy.
+template <int CPL, class Sink>
+__device__ __forceinline__ void filter_tile(const SearchArgs& a, const uint8_t* buf, const uint32_t* tbl,
+                                            uint32_t cw0, int lane, uint16_t* qc, bool edge, int32_t rlo,
+                                            int32_t rhi, Sink& sink) {
+  constexpr int G = CPL < kGroup ? CPL : kGroup;
+#pragma unroll
+  for (int g0 = 0; g0 < CPL; g0 += G) {
+    uint32_t qlen = 0;
+#pragma unroll
+    for (int it = g0; it < g0 + G; ++it) {
+      const uint32_t c = cw0 + it * 32u + lane;
+      const bool hit = chunk_hit(lds128(buf + a.pre + 16u * c), a.bc1);
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, hit);
+      if (hit) qc[qlen + __popc(bal & lanemask_lt())] = (uint16_t)c;
+      qlen += __popc(bal);
+    }
+    __syncwarp();
+    for (uint32_t b0 = 0; b0 < qlen; b0 += 32) {
+      const uint32_t i = b0 + lane;
+      uint32_t c = 0, g = 0;
+      if (i < qlen) {
+        c = qc[i];
+        g = filter_entry(a, buf, tbl, c, edge, rlo, rhi);
+      }
+      if (a.m >= 3) g = verify_survivors(a, buf, tbl, c, g, lane);
+      sink(c, g, lane);
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// the kernel
+// ---------------------------------------------------------------------------
+// Chunk c of a tile covers tile-relative positions u in [16c, 16c+16); warp w owns
+// the contiguous chunks [w*32*CPL, (w+1)*32*CPL), lane l the chunks w*32*CPL +
+// it*32 + l (16-B interleave: conflict-free LDS.128).  For FILTER, u indexes the
+// pi(1)-bytes y = kT + u, i.e. alignment x = kT - a1 + u; for BLOCK, x = kT + u.
+template <int STRAT, int EPI, int MAXM, int CPL>
+__global__ void __launch_bounds__(kThreads, 2) search_kernel(const SearchArgs a, const PatternTable<MAXM> pt) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + kMaxStages;
+  uint32_t* s_wt = reinterpret_cast<uint32_t*>(smem + kWarpTotOff);  // [2][W]
+  uint32_t* tbl = reinterpret_cast<uint32_t*>(smem + kTblOff);
+  uint8_t* ring = smem + a.ring_off;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (uint32_t q = threadIdx.x; q < a.m; q += blockDim.x) tbl[q] = pt.e[q];
+  if (threadIdx.x == 0) {
+    for (uint32_t s = 0; s < a.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    if (lane == 0) produce<EPI>(a, ring, full, empty);
+    return;
+  }
+
+  uint16_t* qc = reinterpret_cast<uint16_t*>(smem + kQueueOff) + warp * kQueueLen;
+  const uint32_t T = a.tile;
+  const int64_t shift = (STRAT == kFilter) ? (int64_t)a.a1 : 0;
+  const uint32_t cw0 = (uint32_t)warp * 32u * CPL;  // first chunk of this warp
+  CountSink total;
+  uint32_t s = 0, ph = 0, par = 0;
+  for (uint64_t ti = blockIdx.x; ti < a.ntiles; ti += gridDim.x) {
+    if (EPI == kEpiWrite && a.tile_offsets[ti + 1] == a.tile_offsets[ti]) continue;
+    mbar_wait(&full[s], ph);
+    const uint8_t* buf = ring + (size_t)s * a.stage_stride;
+    const bool edge = ti < a.edge_lo || ti >= a.edge_hi;  // tile holds invalid alignments
+    int32_t rlo = 0, rhi = (int32_t)T;
+    const int64_t x_base = (int64_t)((a.k_begin + ti) * T) - shift;  // alignment offset of u = 0
+    if (edge) {
+      const int64_t vlo = (int64_t)a.delta, vhi = (int64_t)(a.delta + a.A);
+      rlo = (int32_t)imin(imax(vlo - x_base, 0), (int64_t)T);
+      rhi = (int32_t)imin(imax(vhi - x_base, 0), (int64_t)T);
+    }
+
+    if (STRAT == kFilter) {
+      if (EPI != kEpiWrite) {
+        CountSink cs;
+        filter_tile<CPL>(a, buf, tbl, cw0, lane, qc, edge, rlo, rhi, cs);
+        if (EPI == kEpiCount) {
+          total.n += cs.n;
+        } else {
+          const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, cs.n);
+          if (lane == 0 && ws)
+            atomicAdd(reinterpret_cast<unsigned long long*>(&a.tile_counts[ti]), (unsigned long long)ws);
+        }
+      } else {  // two passes: this warp's total, then ranked writes
+        CountSink cs;
+        filter_tile<CPL>(a, buf, tbl, cw0, lane, qc, edge, rlo, rhi, cs);
+        const uint32_t wtot = __reduce_add_sync(0xFFFFFFFFu, cs.n);
+        if (lane == 0) s_wt[par * kConsumerWarps + warp] = wtot;
+        named_bar_sync(1, kConsumerWarps * 32);
+        WriteSink ws{a.tile_offsets[ti], x_base - (int64_t)a.delta, a.pos, a.cap};
+        for (int w = 0; w < warp; ++w) ws.run += s_wt[par * kConsumerWarps + w];
+        filter_tile<CPL>(a, buf, tbl, cw0, lane, qc, edge, rlo, rhi, ws);
+        par ^= 1u;
+      }
+    } else {
+      Found4 F[CPL];
+#pragma unroll
+      for (int it = 0; it < CPL; ++it)
+        F[it] = edge ? found_from_mask16(range_mask16_rel((int32_t)(16u * (cw0 + it * 32u + lane)), rlo, rhi))
+                     : found_all();
+      uint32_t k = 0;
+      for (; k < a.r; ++k) {  // peeled: all r comparisons, no test
+        const uint32_t e = tbl[k];
+        const uint32_t off = e & 0xFFFFu, bc = (e >> 16) * 0x01010101u;
+#pragma unroll
+        for (int it = 0; it < CPL; ++it)
+          found_and_eq(F[it], load_window16(buf + 16u * (cw0 + it * 32u + lane) + (off & ~15u), off), bc);
+      }
+      for (; k < a.m; ++k) {  // ordered loop with exit test, warp-uniform
+        uint32_t any = 0;
+#pragma unroll
+        for (int it = 0; it < CPL; ++it) any |= found_any(F[it]);
+        if (!__any_sync(0xFFFFFFFFu, any != 0)) break;
+        const uint32_t e = tbl[k];
+        const uint32_t off = e & 0xFFFFu, bc = (e >> 16) * 0x01010101u;
+#pragma unroll
+        for (int it = 0; it < CPL; ++it)
+          found_and_eq(F[it], load_window16(buf + 16u * (cw0 + it * 32u + lane) + (off & ~15u), off), bc);
+      }
+      if (EPI != kEpiWrite) {
+        uint32_t tc = 0;
+#pragma unroll
+        for (int it = 0; it < CPL; ++it)  // popcount of found
+          tc += __popc(compress_found(F[it]));
+        if (EPI == kEpiCount) {
+          total.n += tc;
+        } else {
+          const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, tc);
+          if (lane == 0 && ws)
+            atomicAdd(reinterpret_cast<unsigned long long*>(&a.tile_counts[ti]), (unsigned long long)ws);
+        }
+      } else {
+        uint32_t mk[CPL], tc = 0;
+#pragma unroll
+        for (int it = 0; it < CPL; ++it) {
+          mk[it] = compress_found(F[it]);
+          tc += __popc(mk[it]);
+        }
+        const uint32_t wtot = __reduce_add_sync(0xFFFFFFFFu, tc);
+        if (lane == 0) s_wt[par * kConsumerWarps + warp] = wtot;
+        named_bar_sync(1, kConsumerWarps * 32);
+        WriteSink ws{a.tile_offsets[ti], x_base - (int64_t)a.delta, a.pos, a.cap};
+        for (int w = 0; w < warp; ++w) ws.run += s_wt[par * kConsumerWarps + w];
+#pragma unroll
+        for (int it = 0; it < CPL; ++it) ws(cw0 + it * 32u + lane, mk[it], lane);
+        par ^= 1u;
+      }
+    }
+
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (++s == a.stages) {
+      s = 0;
+      ph ^= 1u;
+    }
+  }
+
+  if (EPI == kEpiCount) {
+    const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, total.n);
+    if (lane == 0 && ws) atomicAdd(reinterpret_cast<unsigned long long*>(a.count_out), (unsigned long long)ws);
+  }
+}
+
+}  // namespace smgpu
