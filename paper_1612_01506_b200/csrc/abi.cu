@@ -118,7 +118,7 @@ struct Tunables {
   uint32_t tile = 32768;        // text bytes per tile for large texts (4096 * CPL)
   int ctas_per_sm = 2;          // persistent CTAs per SM
   uint32_t max_stages = 8;      // ring depth cap per CTA
-  double filter_max_f = 0.10;   // AUTO: FILTER when the rarest pattern symbol has frequency <= this
+  double filter_max_f = 0;      // AUTO: override of the FILTER threshold on f(pi(1)) (0 = built-in)
 };
 
 const Tunables& tunables() {
@@ -166,11 +166,21 @@ sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist
   double total = 0;
   for (int c = 0; c < 256; ++c) total += (double)hist[c];
   auto freq = [&](size_t k) { return total > 0 ? (double)hist[p[pl.order[k]]] / total : 0.0; };
-  if (strategy == SM_STRATEGY_AUTO) strategy = freq(0) <= tunables().filter_max_f ? kFilter : kBlock;
+  if (strategy == SM_STRATEGY_AUTO) {
+    // FILTER's cost grows with the share of 16-byte chunks holding p[pi(1)]; BLOCK's
+    // with the number of packed-byte steps.  Crossovers measured on B200
+    // (tools/strat_cmp.py, profiles/strategy_r1.md): m <= 2 -> BLOCK above f1 ~ 3.5%;
+    // m >= 3 -> BLOCK above f1 ~ 6%.
+    const double f1 = freq(0);
+    const double thr = tunables().filter_max_f > 0 ? tunables().filter_max_f : (m <= 2 ? 0.035 : 0.06);
+    strategy = f1 <= thr ? kFilter : kBlock;
+  }
   pl.strategy = strategy;
   if (peel == 0) {
-    // smallest r with alpha_eff * prod_{k<r} f(pi(k)) <= 1/2 (PAPER.md:176-178 reasoning at alpha_eff)
-    double surv = 32.0 * 16.0 * pl.cpl;
+    // smallest r with alpha_eff * prod_{k<r} f(pi(k)) <= 1/2: the paper's reasoning
+    // for r ("it is less probable that all the alpha comparisons
+    // fail at the same time") at the warp's alpha_eff = 32 lanes x 16 x CPL, capped at 2048.
+    double surv = std::min(32.0 * 16.0 * pl.cpl, 2048.0);
     uint32_t r = 0;
     while (r < m && surv > 0.5) surv *= freq(r++);
     peel = r < 1 ? 1 : r;

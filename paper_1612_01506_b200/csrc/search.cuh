@@ -12,6 +12,7 @@ constexpr int kMaxStages = 8;
 constexpr int kMaxCPL = 8;                               // chunks per lane per tile (tile <= 32 KiB)
 constexpr int kGroup = 8;                                // FILTER: chunk-rows per queue fill
 constexpr int kQueueLen = 32 * kGroup;                   // FILTER: queue entries per warp
+constexpr uint32_t kLaneVerifyMaxM = 34;                 // FILTER: per-lane verification up to this m
 // shared-memory layout: [full/empty mbarriers][warp totals [2][W]][queue chunk ids u16 [W][kQueueLen]][table][ring]
 constexpr uint32_t kWarpTotOff = 2 * kMaxStages * 8;
 constexpr uint32_t kQueueOff = kWarpTotOff + 2 * kConsumerWarps * 4;

@@ -195,12 +195,31 @@ __device__ __forceinline__ uint32_t filter_entry(const SearchArgs& a, const uint
 }
 
 // pi(3..m) for the survivors of pi(1), pi(2) held by the lanes of a warp (g = 0 on
-// lanes without).  Survivors are rare, so the whole warp verifies one at a time:
+// lanes without).  Long patterns: survivors are rare, so the whole warp verifies one at a time:
 // each step compares 32 consecutive positions of the order pi in parallel and
 // exits at the first step with a mismatch (Alg. 3's early exit with 32 pattern
 // positions per step; any order gives the same result).
 __device__ __forceinline__ uint32_t verify_survivors(const SearchArgs& a, const uint8_t* buf, const uint32_t* tbl,
                                                      uint32_t c, uint32_t g, int lane) {
+  if (a.m <= kLaneVerifyMaxM) {
+    // short patterns: each lane checks its own survivors, pi(3..m) in order with
+    // early exit (Alg. 3's inner loop at alpha = 1); at most m - 2 <= 32 steps
+    uint32_t todo = g;
+    const uint8_t* xb = buf + a.pre + 16u * c - a.a1;
+    while (todo) {
+      const uint32_t p = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint8_t* xp = xb + gbit_to_alignment(p);
+      for (uint32_t q = 2; q < a.m; ++q) {
+        const uint32_t e = tbl[q];
+        if (xp[e & 0xFFFFu] != (e >> 16)) {
+          g &= ~(1u << p);
+          break;
+        }
+      }
+    }
+    return g;
+  }
   uint32_t todo = __ballot_sync(0xFFFFFFFFu, g != 0);
   while (todo) {
     const int src = __ffs(todo) - 1;
