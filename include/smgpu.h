@@ -128,6 +128,19 @@ sm_status sm_count_async(const uint8_t* p, size_t m, const uint8_t* t, size_t n,
                          const uint64_t* hist, const uint32_t* order, uint32_t peel,
                          int strategy, uint64_t* d_count, void* stream);
 
+/* Enqueue the counts of P patterns p[i] (host, lengths m[i]) in one device text:
+ * d_counts[i] (DEVICE u64[P], overwritten) = number of occurrences of p[i] starting
+ * at alignments i < min(n - m[i] + 1, max_alignments) -- pass SIZE_MAX to count
+ * all of them; a smaller value counts exactly the alignments a text shard owns
+ * (the bytes past them are its halo).  Each pattern is still a
+ * full pass over the text (no sharing of reads between patterns); batching only
+ * lets the persistent kernel flow from one pattern's last tiles into the next
+ * pattern's first tiles and amortises launch overhead.  hist: as in
+ * sm_count_async; order and peeling factor are chosen per pattern (AUTO). */
+sm_status sm_count_batch(const uint8_t* const* p, const size_t* m, size_t P, const uint8_t* t, size_t n,
+                         size_t max_alignments, const uint64_t* hist, int strategy, uint64_t* d_counts,
+                         void* stream);
+
 /* Enqueue the reporting version: the first min(count, cap) ascending
  * positions go to DEVICE pos[0..cap), the total count to DEVICE *d_count.
  * Truncation is detected by the caller (*d_count > cap) after the stream

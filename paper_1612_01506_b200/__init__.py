@@ -13,6 +13,7 @@ Names mirror the ABI:
 * ``sm_histogram(t, out=None)``           -> int64[256] CUDA tensor (async)
 * ``sm_order_from_histogram(hist, p)``    -> list[int]
 * ``sm_count_async(p, t, d_count, ...)``  -> None (enqueued on the current stream)
+* ``sm_count_batch(patterns, t, d_counts, ...)`` -> None (many patterns, few launches)
 * ``sm_report_async(p, t, pos, d_count, ...)``
 * ``sm_plan(p, hist, ...)``               -> (strategy, peel)
 
@@ -37,7 +38,7 @@ STRATEGY_NAMES = {SM_STRATEGY_FILTER: "filter", SM_STRATEGY_BLOCK: "block"}
 
 EXPORTED_SYMBOLS = (
     "sm_count", "sm_report", "sm_symbol_order", "sm_histogram", "sm_order_from_histogram",
-    "sm_count_async", "sm_report_async", "sm_plan", "sm_last_error", "sm_last_error_message",
+    "sm_count_async", "sm_count_batch", "sm_report_async", "sm_plan", "sm_last_error", "sm_last_error_message",
     "sm_clear_error", "sm_status_string", "sm_version", "sm_launch_count",
 )
 
@@ -78,6 +79,8 @@ def load_library(path: str = LIB_PATH):
     lib.sm_order_from_histogram.argtypes = [_vp, _u8p, _sz, _vp]
     lib.sm_count_async.restype = ctypes.c_int
     lib.sm_count_async.argtypes = [_u8p, _sz, _u8p, _sz, _vp, _vp, ctypes.c_uint32, ctypes.c_int, _vp, _vp]
+    lib.sm_count_batch.restype = ctypes.c_int
+    lib.sm_count_batch.argtypes = [_vp, _vp, _sz, _u8p, _sz, _sz, _vp, ctypes.c_int, _vp, _vp]
     lib.sm_report_async.restype = ctypes.c_int
     lib.sm_report_async.argtypes = [_u8p, _sz, _u8p, _sz, _vp, _vp, ctypes.c_uint32, ctypes.c_int, _vp, _sz,
                                     _vp, _vp]
@@ -242,6 +245,34 @@ def sm_count_async(p, t, d_count, hist=None, order: Optional[Sequence[int]] = No
     h, o = _u64_host(hist), _u32_host(order)
     dptr = d_count if isinstance(d_count, int) else d_count.data_ptr()
     s = lib.sm_count_async(pb, m, tp, n, _np_ptr(h), _np_ptr(o), peel, strategy, dptr, _stream(stream))
+    if s != SM_OK:
+        _raise(s)
+
+
+class PatternBatch:
+    """Host-side packing of a list of patterns for sm_count_batch (reusable across calls)."""
+
+    def __init__(self, patterns):
+        self.data = [bytes(p) if not isinstance(p, str) else p.encode("latin-1") for p in patterns]
+        self.P = len(self.data)
+        self._bufs = [ctypes.create_string_buffer(d, max(len(d), 1)) for d in self.data]
+        self.ptrs = (ctypes.c_void_p * max(self.P, 1))(*[ctypes.addressof(x) for x in self._bufs])
+        self.lens = (ctypes.c_size_t * max(self.P, 1))(*[len(d) for d in self.data])
+
+
+def sm_count_batch(patterns, t, d_counts, hist=None, max_alignments: Optional[int] = None,
+                   strategy: int = SM_STRATEGY_AUTO, stream=None) -> None:
+    """Enqueue the counts of all patterns (list or PatternBatch) into int64 CUDA tensor d_counts[P].
+
+    max_alignments: count only alignments i < max_alignments (a shard's owned range)."""
+    lib = load_library()
+    pb = patterns if isinstance(patterns, PatternBatch) else PatternBatch(patterns)
+    tp, n = _text(t)
+    h = _u64_host(hist)
+    lim = (1 << 64) - 1 if max_alignments is None else int(max_alignments)
+    dptr = d_counts if isinstance(d_counts, int) else d_counts.data_ptr()
+    s = lib.sm_count_batch(ctypes.addressof(pb.ptrs), ctypes.addressof(pb.lens), pb.P, tp, n, lim, _np_ptr(h),
+                           strategy, dptr, _stream(stream))
     if s != SM_OK:
         _raise(s)
 

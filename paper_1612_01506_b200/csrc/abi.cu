@@ -144,6 +144,7 @@ struct Plan {
   std::vector<uint32_t> order;
 };
 
+
 void choose_tiling(uint64_t n, Plan& pl) {
   const uint64_t sms = (uint64_t)num_sms();
   pl.tile = tunables().tile;
@@ -204,67 +205,98 @@ sm_status host_hist(const uint8_t* t, size_t n, cudaStream_t st, uint64_t* out) 
   return SM_OK;
 }
 
-// Fill the launch description for plan `pl`.
-void make_args(const Plan& pl, const uint8_t* p, size_t m, const uint8_t* t, size_t n, SearchArgs& a,
-               std::vector<uint32_t>& table, int& grid, size_t& smem) {
-  std::memset(&a, 0, sizeof(a));
-  const uintptr_t tp = reinterpret_cast<uintptr_t>(t);
-  a.base = reinterpret_cast<const uint8_t*>(tp & ~(uintptr_t)15);
-  a.delta = tp & 15;
-  a.n = n;
-  a.A = n - m + 1;
-  a.m = (uint32_t)m;
-  a.r = pl.r;
-  a.tile = pl.tile;
+// Descriptor of one planned pattern (see search.cuh).  `lim` = max alignments to
+// count (SIZE_MAX: all n - m + 1).
+void fill_desc(const Plan& pl, const uint8_t* p, size_t m, uint64_t delta, uint64_t n, uint64_t lim, PatDesc& d,
+               uint32_t tbl_index) {
+  std::memset(&d, 0, sizeof(d));
   const uint64_t T = pl.tile;
-  table.resize(m);
-  for (size_t k = 0; k < m; ++k) table[k] = pl.order[k] | ((uint32_t)p[pl.order[k]] << 16);
+  d.m = (uint32_t)m;
+  d.r = pl.r;
+  d.tbl = tbl_index;
+  d.A = std::min<uint64_t>(n - m + 1, lim);
   if (pl.strategy == kFilter) {
     const uint32_t a1 = pl.order[0];
-    a.a1 = a1;
-    a.bc1 = (uint32_t)p[a1] * 0x01010101u;
-    a.pre = (a1 + 15) & ~15u;
+    d.a1 = a1;
+    d.bc1 = (uint32_t)p[a1] * 0x01010101u;
+    d.pre = (a1 + 15) & ~15u;
     if (m >= 2) {
       const uint32_t a2 = pl.order[1];
-      a.s2 = a.pre + a2 - a1;
-      a.bc2 = (uint32_t)p[a2] * 0x01010101u;
+      d.s2 = d.pre + a2 - a1;
+      d.bc2 = (uint32_t)p[a2] * 0x01010101u;
     }
     // + 16: the pi(2) window of the last chunk reads up to 32 bytes past its base
     const uint32_t post = (((uint32_t)(m - 1 - a1) + 15) & ~15u) + 16;
-    a.stage_len = (uint32_t)T + a.pre + post;
-    a.k_begin = (a.delta + a1) / T;
-    const uint64_t k_end = (a.delta + a.A - 1 + a1) / T + 1;
-    a.ntiles = k_end - a.k_begin;
+    d.stage_len = (uint32_t)T + d.pre + post;
+    d.k_begin = (delta + a1) / T;
+    const uint64_t k_end = (delta + d.A - 1 + a1) / T + 1;
+    d.ntiles = k_end - d.k_begin;
   } else {
-    a.pre = 0;
+    d.pre = 0;
     const uint32_t post = (((uint32_t)m - 1) & ~15u) + 16;
-    a.stage_len = (uint32_t)T + post;
-    a.k_begin = 0;
-    a.ntiles = (a.delta + a.A - 1) / T + 1;
+    d.stage_len = (uint32_t)T + post;
+    d.k_begin = 0;
+    d.ntiles = (delta + d.A - 1) / T + 1;
   }
-  {  // edge tiles: only these need range masks (tile ti covers alignments x_base + [0, T))
-    const uint64_t shift = pl.strategy == kFilter ? a.a1 : 0;
-    const uint64_t first_full = (a.delta + shift + T - 1) / T;  // smallest k with k*T - shift >= delta
-    a.edge_lo = first_full > a.k_begin ? first_full - a.k_begin : 0;
-    const uint64_t kh = (a.delta + a.A + shift) / T;             // smallest k with (k+1)*T - shift > delta + A
-    a.edge_hi = kh > a.k_begin ? kh - a.k_begin : 0;
+  // edge tiles: only these need range masks (tile ti covers alignments x_base + [0, T))
+  const uint64_t shift = pl.strategy == kFilter ? d.a1 : 0;
+  const uint64_t first_full = (delta + shift + T - 1) / T;  // smallest k with k*T - shift >= delta
+  d.edge_lo = first_full > d.k_begin ? first_full - d.k_begin : 0;
+  const uint64_t kh = (delta + d.A + shift) / T;             // smallest k with (k+1)*T - shift > delta + A
+  d.edge_hi = kh > d.k_begin ? kh - d.k_begin : 0;
+}
+
+struct Planned {
+  Plan pl;
+  const uint8_t* p;
+  size_t m;
+  uint64_t* count_out;
+};
+
+// Build one launch over patterns `ps` (same strategy, same tile; <= kMaxBatch, table <= kTableLarge).
+void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_t n, uint64_t lim, int epilogue,
+                  HostLaunch& L) {
+  const uintptr_t tp = reinterpret_cast<uintptr_t>(t);
+  std::memset(&L.a, 0, sizeof(L.a));
+  L.a.base = reinterpret_cast<const uint8_t*>(tp & ~(uintptr_t)15);
+  L.a.delta = tp & 15;
+  L.a.n = n;
+  L.a.tile = ps[0]->pl.tile;
+  L.strategy = ps[0]->pl.strategy;
+  L.cpl = ps[0]->pl.cpl;
+  L.epilogue = epilogue;
+  L.d.resize(ps.size());
+  L.e.clear();
+  uint64_t work = 0;
+  uint32_t max_stage = 0;
+  for (size_t i = 0; i < ps.size(); ++i) {
+    const Planned& q = *ps[i];
+    fill_desc(q.pl, q.p, q.m, L.a.delta, n, lim, L.d[i], (uint32_t)L.e.size());
+    for (size_t k = 0; k < q.m; ++k) L.e.push_back(q.pl.order[k] | ((uint32_t)q.p[q.pl.order[k]] << 16));
+    work += L.d[i].ntiles;
+    L.d[i].work_end = work;
+    L.d[i].count_out = q.count_out;
+    max_stage = std::max(max_stage, L.d[i].stage_len);
   }
-  a.stage_stride = (a.stage_len + 127) & ~127u;
-  a.ring_off = (kTblOff + 4 * (uint32_t)m + 127) & ~127u;
+  L.a.npat = (uint32_t)ps.size();
+  L.a.total_work = work;
+  L.a.tbl_words = (uint32_t)L.e.size();
+  L.a.stage_stride = (max_stage + 127) & ~127u;
+  L.a.ring_off = (kTblOff + 4 * L.a.tbl_words + 127) & ~127u;
   // shared memory per SM: 228 KiB, 1 KiB reserved per resident CTA
   int ctas = tunables().ctas_per_sm;
   uint32_t stages = 0;
   for (; ctas >= 1; --ctas) {
     const uint32_t budget = std::min<uint32_t>(227 * 1024, 233472 / ctas - 1024);
-    stages = budget > a.ring_off ? (budget - a.ring_off) / a.stage_stride : 0;
+    stages = budget > L.a.ring_off ? (budget - L.a.ring_off) / L.a.stage_stride : 0;
     if (stages >= 2) break;
   }
   if (ctas < 1) ctas = 1;
-  a.stages = std::min<uint32_t>(stages, tunables().max_stages);
-  smem = (size_t)a.ring_off + (size_t)a.stages * a.stage_stride;
+  L.a.stages = std::min<uint32_t>(stages, tunables().max_stages);
+  L.smem = (size_t)L.a.ring_off + (size_t)L.a.stages * L.a.stage_stride;
   const uint64_t sms = (uint64_t)num_sms();
-  grid = (int)std::min<uint64_t>(a.ntiles, sms * (uint64_t)ctas);
-  if (grid < 1) grid = 1;
+  L.grid = (int)std::min<uint64_t>(work, sms * (uint64_t)ctas);
+  if (L.grid < 1) L.grid = 1;
 }
 
 sm_status prepare(const uint8_t* p, size_t m, const uint8_t* t, size_t n, const uint64_t* hist,
@@ -279,22 +311,72 @@ sm_status prepare(const uint8_t* p, size_t m, const uint8_t* t, size_t n, const 
   return make_plan(p, m, n, h, order, peel, strategy, pl);
 }
 
+sm_status launch_checked(const HostLaunch& L, cudaStream_t st, const char* what) {
+  SM_CUDA_TRY(launch_search(L, st), what);
+  ++g_launches;
+  return SM_OK;
+}
+
 sm_status enqueue_count(const uint8_t* p, size_t m, const uint8_t* t, size_t n, const uint64_t* hist,
                         const uint32_t* order, uint32_t peel, int strategy, uint64_t* d_count, cudaStream_t st) {
   SM_CUDA_TRY(cudaMemsetAsync(d_count, 0, sizeof(uint64_t), st), "cudaMemsetAsync(count)");
   if (n < m) return SM_OK;  // reading R2: zero alignments
-  Plan pl;
+  Planned q{Plan(), p, m, d_count};
   uint64_t hb[256];
-  sm_status s = prepare(p, m, t, n, hist, order, peel, strategy, st, pl, hb);
+  sm_status s = prepare(p, m, t, n, hist, order, peel, strategy, st, q.pl, hb);
   if (s != SM_OK) return s;
-  SearchArgs a;
-  std::vector<uint32_t> table;
-  int grid;
-  size_t smem;
-  make_args(pl, p, m, t, n, a, table, grid, smem);
-  a.count_out = d_count;
-  SM_CUDA_TRY(launch_search(a, table.data(), pl.strategy, kEpiCount, pl.cpl, grid, smem, st), "search kernel");
-  ++g_launches;
+  HostLaunch L;
+  build_launch({&q}, t, n, UINT64_MAX, kEpiCount, L);
+  return launch_checked(L, st, "search kernel");
+}
+
+// Counts of P patterns over one text in as few launches as the batch limits allow
+// (each launch runs every one of its patterns as a full pass over the text).
+sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t P, const uint8_t* t, size_t n,
+                              uint64_t lim, const uint64_t* hist, int strategy, uint64_t* d_counts,
+                              cudaStream_t st) {
+  if (P == 0) return SM_OK;
+  SM_CUDA_TRY(cudaMemsetAsync(d_counts, 0, P * sizeof(uint64_t), st), "cudaMemsetAsync(counts)");
+  uint64_t hb[256];
+  const uint64_t* h = hist;
+  if (!h) {
+    sm_status s = host_hist(t, n, st, hb);
+    if (s != SM_OK) return s;
+    h = hb;
+  }
+  std::vector<Planned> plans;
+  plans.reserve(P);
+  for (size_t i = 0; i < P; ++i) {
+    if (n < ms[i] || lim == 0) continue;  // count stays 0
+    Planned q{Plan(), ps[i], ms[i], d_counts + i};
+    sm_status s = make_plan(ps[i], ms[i], n, h, nullptr, 0, strategy, q.pl);
+    if (s != SM_OK) return s;
+    plans.push_back(std::move(q));
+  }
+  // group by strategy (kernel template), keep the caller's order inside a group
+  for (int strat : {(int)kFilter, (int)kBlock}) {
+    std::vector<const Planned*> batch;
+    size_t words = 0;
+    auto flush = [&]() -> sm_status {
+      if (batch.empty()) return SM_OK;
+      HostLaunch L;
+      build_launch(batch, t, n, lim, kEpiCount, L);
+      batch.clear();
+      words = 0;
+      return launch_checked(L, st, "search kernel (batch)");
+    };
+    for (const Planned& q : plans) {
+      if (q.pl.strategy != strat) continue;
+      if (batch.size() == (size_t)kMaxBatch || words + q.m > (size_t)kTableLarge) {
+        sm_status s = flush();
+        if (s != SM_OK) return s;
+      }
+      batch.push_back(&q);
+      words += q.m;
+    }
+    sm_status s = flush();
+    if (s != SM_OK) return s;
+  }
   return SM_OK;
 }
 
@@ -303,18 +385,16 @@ sm_status enqueue_report(const uint8_t* p, size_t m, const uint8_t* t, size_t n,
                          uint64_t* d_count, cudaStream_t st) {
   SM_CUDA_TRY(cudaMemsetAsync(d_count, 0, sizeof(uint64_t), st), "cudaMemsetAsync(count)");
   if (n < m) return SM_OK;
-  Plan pl;
+  Planned q{Plan(), p, m, nullptr};
   uint64_t hb[256];
-  sm_status s = prepare(p, m, t, n, hist, order, peel, strategy, st, pl, hb);
+  sm_status s = prepare(p, m, t, n, hist, order, peel, strategy, st, q.pl, hb);
   if (s != SM_OK) return s;
-  SearchArgs a;
-  std::vector<uint32_t> table;
-  int grid;
-  size_t smem;
-  make_args(pl, p, m, t, n, a, table, grid, smem);
+  HostLaunch L;
+  build_launch({&q}, t, n, UINT64_MAX, kEpiTileCount, L);
 
   // scratch: per-tile counts (ntiles + 1, last = 0) and their exclusive prefix
-  const uint64_t nt1 = a.ntiles + 1;
+  const uint64_t ntiles = L.d[0].ntiles;
+  const uint64_t nt1 = ntiles + 1;
   size_t temp_bytes = 0;
   SM_CUDA_TRY(exclusive_scan_u64(nullptr, nullptr, nt1, nullptr, &temp_bytes, st), "scan sizing");
   const size_t off_bytes = ((nt1 * 8 + 255) / 256) * 256;
@@ -326,21 +406,22 @@ sm_status enqueue_report(const uint8_t* p, size_t m, const uint8_t* t, size_t n,
   void* temp = scratch + 2 * off_bytes;
   cudaError_t e = cudaMemsetAsync(counts, 0, nt1 * 8, st);
   if (e == cudaSuccess) {
-    a.tile_counts = counts;
-    e = launch_search(a, table.data(), pl.strategy, kEpiTileCount, pl.cpl, grid, smem, st);  // pass 1
+    L.a.tile_counts = counts;
+    e = launch_search(L, st);  // pass 1: per-tile counts
     if (e == cudaSuccess) ++g_launches;
   }
   if (e == cudaSuccess) {
     e = exclusive_scan_u64(counts, offsets, nt1, temp, &temp_bytes, st);
     if (e == cudaSuccess) g_launches += 1;
   }
-  if (e == cudaSuccess) e = cudaMemcpyAsync(d_count, offsets + a.ntiles, 8, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_count, offsets + ntiles, 8, cudaMemcpyDeviceToDevice, st);
   if (e == cudaSuccess && cap > 0) {
-    a.tile_counts = nullptr;
-    a.tile_offsets = offsets;
-    a.pos = pos;
-    a.cap = cap;
-    e = launch_search(a, table.data(), pl.strategy, kEpiWrite, pl.cpl, grid, smem, st);  // pass 2
+    L.epilogue = kEpiWrite;
+    L.a.tile_counts = nullptr;
+    L.a.tile_offsets = offsets;
+    L.a.pos = pos;
+    L.a.cap = cap;
+    e = launch_search(L, st);  // pass 2: ranked writes in tiles with matches
     if (e == cudaSuccess) ++g_launches;
   }
   cudaFreeAsync(scratch, st);
@@ -452,6 +533,27 @@ sm_status sm_count_async(const uint8_t* p, size_t m, const uint8_t* t, size_t n,
   s = check_device_ptr(d_count, "d_count");
   if (s != SM_OK) return s;
   return enqueue_count(p, m, t, n, hist, order, peel, strategy, d_count, as_stream(stream));
+}
+
+sm_status sm_count_batch(const uint8_t* const* p, const size_t* m, size_t P, const uint8_t* t, size_t n,
+                         size_t max_alignments, const uint64_t* hist, int strategy, uint64_t* d_counts,
+                         void* stream) {
+  if (P == 0) return SM_OK;
+  if (!p || !m || !d_counts) return fail(SM_EINVAL, "NULL argument");
+  if (strategy < SM_STRATEGY_AUTO || strategy > SM_STRATEGY_BLOCK) return fail(SM_EINVAL, "bad strategy");
+  for (size_t i = 0; i < P; ++i) {
+    if (m[i] == 0) return fail(SM_EINVAL, "m[i] == 0: empty pattern is undefined (reading R2)");
+    if (m[i] > SM_MAX_PATTERN) return fail(SM_EINVAL, "m[i] > SM_MAX_PATTERN (4096)");
+    if (!p[i]) return fail(SM_EINVAL, "p[i] is NULL");
+  }
+  if (n > 0) {
+    if (!t) return fail(SM_EINVAL, "t is NULL with n > 0");
+    sm_status s = check_device_ptr(t, "t");
+    if (s != SM_OK) return s;
+  }
+  sm_status s = check_device_ptr(d_counts, "d_counts");
+  if (s != SM_OK) return s;
+  return enqueue_count_batch(p, m, P, t, n, (uint64_t)max_alignments, hist, strategy, d_counts, as_stream(stream));
 }
 
 sm_status sm_report_async(const uint8_t* p, size_t m, const uint8_t* t, size_t n, const uint64_t* hist,

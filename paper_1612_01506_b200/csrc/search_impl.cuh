@@ -37,47 +37,6 @@ __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
 }
 
 // ---------------------------------------------------------------------------
-// TMA producer (one thread)
-// ---------------------------------------------------------------------------
-template <int EPI>
-__device__ void produce(const SearchArgs& a, uint8_t* ring, uint64_t* full, uint64_t* empty) {
-  const uint64_t pol = l2_policy_evict_first();
-  const int64_t tlo = (int64_t)a.delta, thi = (int64_t)(a.delta + a.n);
-  uint32_t s = 0, ph = 0;  // stage and its use parity
-  bool wrapped = false;
-  for (uint64_t ti = blockIdx.x; ti < a.ntiles; ti += gridDim.x) {
-    if (EPI == kEpiWrite && a.tile_offsets[ti + 1] == a.tile_offsets[ti]) continue;
-    if (wrapped) mbar_wait_sleep(&empty[s], ph ^ 1u);  // consumers released this stage's previous use
-    uint8_t* buf = ring + (size_t)s * a.stage_stride;
-    const int64_t lo = (int64_t)((a.k_begin + ti) * a.tile) - (int64_t)a.pre;
-    const int64_t hi = lo + (int64_t)a.stage_len;
-    const int64_t vlo = imax(lo, tlo), vhi = imin(hi, thi);
-    uint32_t tx = 0;
-    int64_t alo = 0;
-    if (vlo < vhi) {
-      alo = (vlo + 15) & ~(int64_t)15;
-      const int64_t ahi = vhi & ~(int64_t)15;
-      bool ragged = false;
-      if (alo < ahi) {
-        for (int64_t o = vlo; o < alo; ++o) { buf[o - lo] = ldg_u8_nc(a.base + o); ragged = true; }
-        for (int64_t o = ahi; o < vhi; ++o) { buf[o - lo] = ldg_u8_nc(a.base + o); ragged = true; }
-        tx = (uint32_t)(ahi - alo);
-      } else {
-        for (int64_t o = vlo; o < vhi; ++o) { buf[o - lo] = ldg_u8_nc(a.base + o); ragged = true; }
-      }
-      if (ragged) fence_proxy_async_smem();
-    }
-    mbar_arrive_expect_tx(&full[s], tx);
-    if (tx) tma_load_1d(buf + (alo - lo), a.base + alo, tx, &full[s], pol);
-    if (++s == a.stages) {
-      s = 0;
-      ph ^= 1u;
-      wrapped = true;
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Packed-byte helpers for one lane-chunk of 16 alignments (4 x u32 flag words,
 // 0x80 per surviving alignment: the sm_100a form of the paper's `found`).
 // ---------------------------------------------------------------------------
@@ -158,6 +117,60 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return r;
 }
 
+// Per-tile view of one pattern of the batch (read from the kernel parameters).
+struct Pat {
+  uint32_t m, r, a1, bc1, s2, bc2, pre;
+  const uint32_t* tbl;  // shared-memory table of this pattern (m entries, pi order)
+};
+
+// ---------------------------------------------------------------------------
+// TMA producer (one thread): for every work item (pattern, tile) of this CTA,
+// wait for a free stage, load the ragged 16-B ends of t byte-wise, then one
+// cp.async.bulk for the aligned interior, completion counted on full[s].
+// ---------------------------------------------------------------------------
+template <int EPI, int CAP>
+__device__ void produce(const LaunchParams<CAP>& P, uint8_t* ring, uint64_t* full, uint64_t* empty) {
+  const LaunchArgs& a = P.a;
+  const uint64_t pol = l2_policy_evict_first();
+  const int64_t tlo = (int64_t)a.delta, thi = (int64_t)(a.delta + a.n);
+  uint32_t s = 0, ph = 0;  // stage and its use parity
+  bool wrapped = false;
+  uint32_t k = 0;
+  for (uint64_t w = blockIdx.x; w < a.total_work; w += gridDim.x) {
+    while (w >= P.d[k].work_end) ++k;
+    const PatDesc& d = P.d[k];
+    const uint64_t ti = w - (d.work_end - d.ntiles);
+    if (EPI == kEpiWrite && a.tile_offsets[ti + 1] == a.tile_offsets[ti]) continue;
+    if (wrapped) mbar_wait_sleep(&empty[s], ph ^ 1u);  // consumers released this stage's previous use
+    uint8_t* buf = ring + (size_t)s * a.stage_stride;
+    const int64_t lo = (int64_t)((d.k_begin + ti) * a.tile) - (int64_t)d.pre;
+    const int64_t hi = lo + (int64_t)d.stage_len;
+    const int64_t vlo = imax(lo, tlo), vhi = imin(hi, thi);
+    uint32_t tx = 0;
+    int64_t alo = 0;
+    if (vlo < vhi) {
+      alo = (vlo + 15) & ~(int64_t)15;
+      const int64_t ahi = vhi & ~(int64_t)15;
+      bool ragged = false;
+      if (alo < ahi) {
+        for (int64_t o = vlo; o < alo; ++o) { buf[o - lo] = ldg_u8_nc(a.base + o); ragged = true; }
+        for (int64_t o = ahi; o < vhi; ++o) { buf[o - lo] = ldg_u8_nc(a.base + o); ragged = true; }
+        tx = (uint32_t)(ahi - alo);
+      } else {
+        for (int64_t o = vlo; o < vhi; ++o) { buf[o - lo] = ldg_u8_nc(a.base + o); ragged = true; }
+      }
+      if (ragged) fence_proxy_async_smem();
+    }
+    mbar_arrive_expect_tx(&full[s], tx);
+    if (tx) tma_load_1d(buf + (alo - lo), a.base + alo, tx, &full[s], pol);
+    if (++s == a.stages) {
+      s = 0;
+      ph ^= 1u;
+      wrapped = true;
+    }
+  }
+}
+
 // FILTER phase A: does any of the 16 pi(1)-bytes of a chunk equal p[pi(1)]?
 // (borrow-based zero-byte test: exact as a whole-chunk predicate)
 __device__ __forceinline__ bool chunk_hit(const uint4 v, uint32_t bc) {
@@ -186,32 +199,30 @@ __device__ __forceinline__ uint32_t g_to_mask16(uint32_t g) {
 // 16 alignments -- exact packed-byte compares of pi(1) and pi(2) without a test
 // in between.  Returns the compressed found word (bit
 // (8k + 7 - i) <-> tile-relative alignment u = 16c + 4i + k) of the survivors.
-__device__ __forceinline__ uint32_t filter_entry(const SearchArgs& a, const uint8_t* buf, const uint32_t* tbl,
-                                                 uint32_t c, bool edge, int32_t rlo, int32_t rhi) {
+__device__ __forceinline__ uint32_t filter_entry(const Pat& pt, const uint8_t* buf, uint32_t c, bool edge,
+                                                 int32_t rlo, int32_t rhi) {
   Found4 F = edge ? found_from_mask16(range_mask16_rel((int32_t)(16u * c), rlo, rhi)) : found_all();
-  found_and_eq(F, lds128(buf + a.pre + 16u * c), a.bc1);                                       // pi(1)
-  if (a.m >= 2) found_and_eq(F, load_window16(buf + 16u * c + (a.s2 & ~15u), a.s2), a.bc2);  // pi(2)
+  found_and_eq(F, lds128(buf + pt.pre + 16u * c), pt.bc1);                                        // pi(1)
+  if (pt.m >= 2) found_and_eq(F, load_window16(buf + 16u * c + (pt.s2 & ~15u), pt.s2), pt.bc2);  // pi(2)
   return compress_found(F);
 }
 
 // pi(3..m) for the survivors of pi(1), pi(2) held by the lanes of a warp (g = 0 on
-// lanes without).  Long patterns: survivors are rare, so the whole warp verifies one at a time:
-// each step compares 32 consecutive positions of the order pi in parallel and
-// exits at the first step with a mismatch (Alg. 3's early exit with 32 pattern
-// positions per step; any order gives the same result).
-__device__ __forceinline__ uint32_t verify_survivors(const SearchArgs& a, const uint8_t* buf, const uint32_t* tbl,
-                                                     uint32_t c, uint32_t g, int lane) {
-  if (a.m <= kLaneVerifyMaxM) {
-    // short patterns: each lane checks its own survivors, pi(3..m) in order with
-    // early exit (Alg. 3's inner loop at alpha = 1); at most m - 2 <= 32 steps
+// lanes without), early exit at the first mismatch (Alg. 3's inner loop; any
+// order gives the same result).  Short patterns: each lane checks
+// its own survivors.  Long patterns: survivors are rare, so the whole warp
+// verifies one at a time, 32 consecutive positions of pi per step.
+__device__ __forceinline__ uint32_t verify_survivors(const Pat& pt, const uint8_t* buf, uint32_t c, uint32_t g,
+                                                     int lane) {
+  if (pt.m <= kLaneVerifyMaxM) {
     uint32_t todo = g;
-    const uint8_t* xb = buf + a.pre + 16u * c - a.a1;
+    const uint8_t* xb = buf + pt.pre + 16u * c - pt.a1;  // smem address of alignment u = 16c
     while (todo) {
       const uint32_t p = __ffs(todo) - 1;
       todo &= todo - 1;
       const uint8_t* xp = xb + gbit_to_alignment(p);
-      for (uint32_t q = 2; q < a.m; ++q) {
-        const uint32_t e = tbl[q];
+      for (uint32_t q = 2; q < pt.m; ++q) {
+        const uint32_t e = pt.tbl[q];
         if (xp[e & 0xFFFFu] != (e >> 16)) {
           g &= ~(1u << p);
           break;
@@ -227,16 +238,16 @@ __device__ __forceinline__ uint32_t verify_survivors(const SearchArgs& a, const 
     uint32_t gs = __shfl_sync(0xFFFFFFFFu, g, src);
     const uint32_t cs = __shfl_sync(0xFFFFFFFFu, c, src);
     uint32_t keep = gs;
-    const uint8_t* xb = buf + a.pre + 16u * cs - a.a1;  // smem address of alignment u = 16 cs
+    const uint8_t* xb = buf + pt.pre + 16u * cs - pt.a1;
     while (gs) {
       const uint32_t p = __ffs(gs) - 1;
       gs &= gs - 1;
       const uint8_t* xp = xb + gbit_to_alignment(p);
-      for (uint32_t q0 = 2; q0 < a.m; q0 += 32) {
+      for (uint32_t q0 = 2; q0 < pt.m; q0 += 32) {
         const uint32_t q = q0 + lane;
         bool mis = false;
-        if (q < a.m) {
-          const uint32_t e = tbl[q];
+        if (q < pt.m) {
+          const uint32_t e = pt.tbl[q];
           mis = xp[e & 0xFFFFu] != (e >> 16);
         }
         if (__any_sync(0xFFFFFFFFu, mis)) {
@@ -256,8 +267,8 @@ struct WriteSink {
   int64_t pbase;   // 0-based position of u = 0
   uint64_t* pos;
   uint64_t cap;
-  __device__ __forceinline__ void operator()(uint32_t c, uint32_t m16, int lane) {
-    m16 = g_to_mask16(m16);
+  __device__ __forceinline__ void operator()(uint32_t c, uint32_t g, int lane) {
+    uint32_t m16 = g_to_mask16(g);
     const uint32_t pc = __popc(m16);
     const uint32_t incl = warp_incl_scan(pc, lane);
     uint64_t idx = run + incl - pc;
@@ -273,7 +284,7 @@ struct WriteSink {
 
 struct CountSink {
   uint32_t n = 0;
-  __device__ __forceinline__ void operator()(uint32_t, uint32_t m16, int) { n += __popc(m16); }
+  __device__ __forceinline__ void operator()(uint32_t, uint32_t g, int) { n += __popc(g); }
 };
 
 // One warp's share of a FILTER tile, in groups of kGroup chunk-rows: phase A
@@ -281,9 +292,8 @@ struct CountSink {
 // queue (ascending chunk order); phase B drains it 32 entries at a time, one
 // chunk per lane, all lanes busy.
 template <int CPL, class Sink>
-__device__ __forceinline__ void filter_tile(const SearchArgs& a, const uint8_t* buf, const uint32_t* tbl,
-                                            uint32_t cw0, int lane, uint16_t* qc, bool edge, int32_t rlo,
-                                            int32_t rhi, Sink& sink) {
+__device__ __forceinline__ void filter_tile(const Pat& pt, const uint8_t* buf, uint32_t cw0, int lane, uint16_t* qc,
+                                            bool edge, int32_t rlo, int32_t rhi, Sink& sink) {
   constexpr int G = CPL < kGroup ? CPL : kGroup;
 #pragma unroll
   for (int g0 = 0; g0 < CPL; g0 += G) {
@@ -291,7 +301,7 @@ __device__ __forceinline__ void filter_tile(const SearchArgs& a, const uint8_t* 
 #pragma unroll
     for (int it = g0; it < g0 + G; ++it) {
       const uint32_t c = cw0 + it * 32u + lane;
-      const bool hit = chunk_hit(lds128(buf + a.pre + 16u * c), a.bc1);
+      const bool hit = chunk_hit(lds128(buf + pt.pre + 16u * c), pt.bc1);
       const uint32_t bal = __ballot_sync(0xFFFFFFFFu, hit);
       if (hit) qc[qlen + __popc(bal & lanemask_lt())] = (uint16_t)c;
       qlen += __popc(bal);
@@ -302,27 +312,58 @@ __device__ __forceinline__ void filter_tile(const SearchArgs& a, const uint8_t* 
       uint32_t c = 0, g = 0;
       if (i < qlen) {
         c = qc[i];
-        g = filter_entry(a, buf, tbl, c, edge, rlo, rhi);
+        g = filter_entry(pt, buf, c, edge, rlo, rhi);
       }
-      if (a.m >= 3) g = verify_survivors(a, buf, tbl, c, g, lane);
+      if (pt.m >= 3) g = verify_survivors(pt, buf, c, g, lane);
       sink(c, g, lane);
     }
     __syncwarp();
   }
 }
 
+// One warp's share of a BLOCK tile: Alg. 4 on 16 alignments per lane-chunk.
+template <int CPL>
+__device__ __forceinline__ void block_tile(const Pat& pt, const uint8_t* buf, uint32_t cw0, int lane, bool edge,
+                                           int32_t rlo, int32_t rhi, uint32_t* g_out) {
+  Found4 F[CPL];
+#pragma unroll
+  for (int it = 0; it < CPL; ++it)
+    F[it] = edge ? found_from_mask16(range_mask16_rel((int32_t)(16u * (cw0 + it * 32u + lane)), rlo, rhi))
+                 : found_all();
+  uint32_t k = 0;
+  for (; k < pt.r; ++k) {  // peeled: all r comparisons, no test
+    const uint32_t e = pt.tbl[k];
+    const uint32_t off = e & 0xFFFFu, bc = (e >> 16) * 0x01010101u;
+#pragma unroll
+    for (int it = 0; it < CPL; ++it)
+      found_and_eq(F[it], load_window16(buf + 16u * (cw0 + it * 32u + lane) + (off & ~15u), off), bc);
+  }
+  for (; k < pt.m; ++k) {  // ordered loop with exit test, warp-uniform
+    uint32_t any = 0;
+#pragma unroll
+    for (int it = 0; it < CPL; ++it) any |= found_any(F[it]);
+    if (!__any_sync(0xFFFFFFFFu, any != 0)) break;
+    const uint32_t e = pt.tbl[k];
+    const uint32_t off = e & 0xFFFFu, bc = (e >> 16) * 0x01010101u;
+#pragma unroll
+    for (int it = 0; it < CPL; ++it)
+      found_and_eq(F[it], load_window16(buf + 16u * (cw0 + it * 32u + lane) + (off & ~15u), off), bc);
+  }
+#pragma unroll
+  for (int it = 0; it < CPL; ++it) g_out[it] = compress_found(F[it]);  // popcount of found
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
-// the kernel
+// the kernel: a batch of patterns, each a full pass over the text; work item w
+// = (pattern k, tile ti) in pattern-major order, round-robin over persistent CTAs
+// (one CTA flows from one pattern's last tiles into the next pattern's first).
 // ---------------------------------------------------------------------------
-// Chunk c of a tile covers tile-relative positions u in [16c, 16c+16); warp w owns
-// the contiguous chunks [w*32*CPL, (w+1)*32*CPL), lane l the chunks w*32*CPL +
-// it*32 + l (16-B interleave: conflict-free LDS.128).  For FILTER, u indexes the
-// pi(1)-bytes y = kT + u, i.e. alignment x = kT - a1 + u; for BLOCK, x = kT + u.
-template <int STRAT, int EPI, int MAXM, int CPL>
-__global__ void __launch_bounds__(kThreads, 2) search_kernel(const SearchArgs a, const PatternTable<MAXM> pt) {
+template <int STRAT, int EPI, int CAP, int CPL>
+__global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_constant__ LaunchParams<CAP> P) {
   extern __shared__ __align__(128) uint8_t smem[];
+  const LaunchArgs& a = P.a;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + kMaxStages;
   uint32_t* s_wt = reinterpret_cast<uint32_t*>(smem + kWarpTotOff);  // [2][W]
@@ -330,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const SearchArgs a,
   uint8_t* ring = smem + a.ring_off;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (uint32_t q = threadIdx.x; q < a.m; q += blockDim.x) tbl[q] = pt.e[q];
+  for (uint32_t q = threadIdx.x; q < a.tbl_words; q += blockDim.x) tbl[q] = P.e[q];
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < a.stages; ++s) {
       mbar_init(&full[s], 1);
@@ -341,25 +382,37 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const SearchArgs a,
   __syncthreads();
 
   if (warp == kConsumerWarps) {
-    if (lane == 0) produce<EPI>(a, ring, full, empty);
+    if (lane == 0) produce<EPI>(P, ring, full, empty);
     return;
   }
 
   uint16_t* qc = reinterpret_cast<uint16_t*>(smem + kQueueOff) + warp * kQueueLen;
   const uint32_t T = a.tile;
-  const int64_t shift = (STRAT == kFilter) ? (int64_t)a.a1 : 0;
   const uint32_t cw0 = (uint32_t)warp * 32u * CPL;  // first chunk of this warp
-  CountSink total;
   uint32_t s = 0, ph = 0, par = 0;
-  for (uint64_t ti = blockIdx.x; ti < a.ntiles; ti += gridDim.x) {
+  uint32_t k = 0;
+  uint32_t acc = 0;  // kEpiCount: this lane's matches of pattern k so far
+  for (uint64_t w = blockIdx.x; w < a.total_work; w += gridDim.x) {
+    while (w >= P.d[k].work_end) {
+      if (EPI == kEpiCount) {  // flush pattern k (warp-uniform)
+        const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, acc);
+        if (lane == 0 && ws) atomicAdd(reinterpret_cast<unsigned long long*>(P.d[k].count_out), (unsigned long long)ws);
+        acc = 0;
+      }
+      ++k;
+    }
+    const PatDesc& d = P.d[k];
+    const uint64_t ti = w - (d.work_end - d.ntiles);
     if (EPI == kEpiWrite && a.tile_offsets[ti + 1] == a.tile_offsets[ti]) continue;
     mbar_wait(&full[s], ph);
     const uint8_t* buf = ring + (size_t)s * a.stage_stride;
-    const bool edge = ti < a.edge_lo || ti >= a.edge_hi;  // tile holds invalid alignments
+    const Pat pt{d.m, d.r, d.a1, d.bc1, d.s2, d.bc2, d.pre, tbl + d.tbl};
+    const bool edge = ti < d.edge_lo || ti >= d.edge_hi;  // tile holds invalid alignments
+    const int64_t shift = (STRAT == kFilter) ? (int64_t)d.a1 : 0;
+    const int64_t x_base = (int64_t)((d.k_begin + ti) * T) - shift;  // alignment offset of u = 0
     int32_t rlo = 0, rhi = (int32_t)T;
-    const int64_t x_base = (int64_t)((a.k_begin + ti) * T) - shift;  // alignment offset of u = 0
     if (edge) {
-      const int64_t vlo = (int64_t)a.delta, vhi = (int64_t)(a.delta + a.A);
+      const int64_t vlo = (int64_t)a.delta, vhi = (int64_t)(a.delta + d.A);
       rlo = (int32_t)imin(imax(vlo - x_base, 0), (int64_t)T);
       rhi = (int32_t)imin(imax(vhi - x_base, 0), (int64_t)T);
     }
@@ -367,9 +420,9 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const SearchArgs a,
     if (STRAT == kFilter) {
       if (EPI != kEpiWrite) {
         CountSink cs;
-        filter_tile<CPL>(a, buf, tbl, cw0, lane, qc, edge, rlo, rhi, cs);
+        filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, cs);
         if (EPI == kEpiCount) {
-          total.n += cs.n;
+          acc += cs.n;
         } else {
           const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, cs.n);
           if (lane == 0 && ws)
@@ -377,66 +430,35 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const SearchArgs a,
         }
       } else {  // two passes: this warp's total, then ranked writes
         CountSink cs;
-        filter_tile<CPL>(a, buf, tbl, cw0, lane, qc, edge, rlo, rhi, cs);
+        filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, cs);
         const uint32_t wtot = __reduce_add_sync(0xFFFFFFFFu, cs.n);
         if (lane == 0) s_wt[par * kConsumerWarps + warp] = wtot;
         named_bar_sync(1, kConsumerWarps * 32);
         WriteSink ws{a.tile_offsets[ti], x_base - (int64_t)a.delta, a.pos, a.cap};
-        for (int w = 0; w < warp; ++w) ws.run += s_wt[par * kConsumerWarps + w];
-        filter_tile<CPL>(a, buf, tbl, cw0, lane, qc, edge, rlo, rhi, ws);
+        for (int wv = 0; wv < warp; ++wv) ws.run += s_wt[par * kConsumerWarps + wv];
+        filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, ws);
         par ^= 1u;
       }
     } else {
-      Found4 F[CPL];
+      uint32_t g[CPL];
+      block_tile<CPL>(pt, buf, cw0, lane, edge, rlo, rhi, g);
+      uint32_t tc = 0;
 #pragma unroll
-      for (int it = 0; it < CPL; ++it)
-        F[it] = edge ? found_from_mask16(range_mask16_rel((int32_t)(16u * (cw0 + it * 32u + lane)), rlo, rhi))
-                     : found_all();
-      uint32_t k = 0;
-      for (; k < a.r; ++k) {  // peeled: all r comparisons, no test
-        const uint32_t e = tbl[k];
-        const uint32_t off = e & 0xFFFFu, bc = (e >> 16) * 0x01010101u;
-#pragma unroll
-        for (int it = 0; it < CPL; ++it)
-          found_and_eq(F[it], load_window16(buf + 16u * (cw0 + it * 32u + lane) + (off & ~15u), off), bc);
-      }
-      for (; k < a.m; ++k) {  // ordered loop with exit test, warp-uniform
-        uint32_t any = 0;
-#pragma unroll
-        for (int it = 0; it < CPL; ++it) any |= found_any(F[it]);
-        if (!__any_sync(0xFFFFFFFFu, any != 0)) break;
-        const uint32_t e = tbl[k];
-        const uint32_t off = e & 0xFFFFu, bc = (e >> 16) * 0x01010101u;
-#pragma unroll
-        for (int it = 0; it < CPL; ++it)
-          found_and_eq(F[it], load_window16(buf + 16u * (cw0 + it * 32u + lane) + (off & ~15u), off), bc);
-      }
-      if (EPI != kEpiWrite) {
-        uint32_t tc = 0;
-#pragma unroll
-        for (int it = 0; it < CPL; ++it)  // popcount of found
-          tc += __popc(compress_found(F[it]));
-        if (EPI == kEpiCount) {
-          total.n += tc;
-        } else {
-          const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, tc);
-          if (lane == 0 && ws)
-            atomicAdd(reinterpret_cast<unsigned long long*>(&a.tile_counts[ti]), (unsigned long long)ws);
-        }
+      for (int it = 0; it < CPL; ++it) tc += __popc(g[it]);
+      if (EPI == kEpiCount) {
+        acc += tc;
+      } else if (EPI == kEpiTileCount) {
+        const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, tc);
+        if (lane == 0 && ws)
+          atomicAdd(reinterpret_cast<unsigned long long*>(&a.tile_counts[ti]), (unsigned long long)ws);
       } else {
-        uint32_t mk[CPL], tc = 0;
-#pragma unroll
-        for (int it = 0; it < CPL; ++it) {
-          mk[it] = compress_found(F[it]);
-          tc += __popc(mk[it]);
-        }
         const uint32_t wtot = __reduce_add_sync(0xFFFFFFFFu, tc);
         if (lane == 0) s_wt[par * kConsumerWarps + warp] = wtot;
         named_bar_sync(1, kConsumerWarps * 32);
         WriteSink ws{a.tile_offsets[ti], x_base - (int64_t)a.delta, a.pos, a.cap};
-        for (int w = 0; w < warp; ++w) ws.run += s_wt[par * kConsumerWarps + w];
+        for (int wv = 0; wv < warp; ++wv) ws.run += s_wt[par * kConsumerWarps + wv];
 #pragma unroll
-        for (int it = 0; it < CPL; ++it) ws(cw0 + it * 32u + lane, mk[it], lane);
+        for (int it = 0; it < CPL; ++it) ws(cw0 + it * 32u + lane, g[it], lane);
         par ^= 1u;
       }
     }
@@ -450,8 +472,8 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const SearchArgs a,
   }
 
   if (EPI == kEpiCount) {
-    const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, total.n);
-    if (lane == 0 && ws) atomicAdd(reinterpret_cast<unsigned long long*>(a.count_out), (unsigned long long)ws);
+    const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, acc);
+    if (lane == 0 && ws) atomicAdd(reinterpret_cast<unsigned long long*>(P.d[k].count_out), (unsigned long long)ws);
   }
 }
 

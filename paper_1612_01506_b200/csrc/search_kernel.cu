@@ -3,15 +3,12 @@
 
 namespace smgpu {
 
-cudaError_t launch_search_filter(const SearchArgs& a, const uint32_t* table, int epilogue, int cpl, int grid,
-                                 size_t smem_bytes, cudaStream_t stream);
-cudaError_t launch_search_block(const SearchArgs& a, const uint32_t* table, int epilogue, int cpl, int grid,
-                                size_t smem_bytes, cudaStream_t stream);
+cudaError_t launch_search_filter(const HostLaunch& L, cudaStream_t st);
+cudaError_t launch_search_block(const HostLaunch& L, cudaStream_t st);
 
-cudaError_t launch_search(const SearchArgs& a, const uint32_t* table, int strategy, int epilogue, int cpl,
-                          int grid, size_t smem_bytes, cudaStream_t stream) {
-  if (strategy == kFilter) return launch_search_filter(a, table, epilogue, cpl, grid, smem_bytes, stream);
-  return launch_search_block(a, table, epilogue, cpl, grid, smem_bytes, stream);
+cudaError_t launch_search(const HostLaunch& L, cudaStream_t st) {
+  if (L.strategy == kFilter) return launch_search_filter(L, st);
+  return launch_search_block(L, st);
 }
 
 }  // namespace smgpu

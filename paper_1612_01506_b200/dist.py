@@ -88,16 +88,18 @@ def global_histogram(shard_text, shard: Shard, group=None, stream=None):
 
 
 def count_sharded(patterns, shard_text, shard: Shard, hist, counts=None, group=None, stream=None,
-                  peel: int = 0, strategy: int = 0):
-    """Global counts of each pattern: local kernel launches + one all_reduce of int64[P]."""
+                  strategy: int = 0):
+    """Global counts of each pattern: batched local launches over the rank's held bytes,
+    counting only its owned alignments, + one all_reduce of int64[P]."""
     import torch
 
     import paper_1612_01506_b200 as sm
-    P = len(patterns)
+    pb = patterns if isinstance(patterns, sm.PatternBatch) else sm.PatternBatch(patterns)
     if counts is None:
-        counts = torch.zeros(max(P, 1), dtype=torch.int64, device=shard_text.device)
-    for i, p in enumerate(patterns):
-        L = shard.view_len(len(p))
-        sm.sm_count_async(p, shard_text[:L], counts[i:i + 1], hist=hist, peel=peel, strategy=strategy,
-                          stream=stream)
+        counts = torch.zeros(max(pb.P, 1), dtype=torch.int64, device=shard_text.device)
+    max_m = max((len(p) for p in pb.data), default=1)
+    shard.view_len(max_m)  # halo check
+    held = shard_text[: shard.held_len]
+    sm.sm_count_batch(pb, held, counts, hist=hist, max_alignments=shard.owned_bytes, strategy=strategy,
+                      stream=stream)
     return allreduce_sum_(counts, group)

@@ -256,3 +256,60 @@ def test_virtual_shards_sum(sm):
                     view = t[sh.own_lo: sh.own_lo + sh.view_len(m)]
                     tot += count_async(sm, p, view)
                 assert tot == want, (m, G)
+
+
+# ------------------------------------------------------------------------------------------- batched launches
+def test_count_batch_matches_oracle(sm):
+    rng = np.random.default_rng(77)
+    for sigma, n in ((256, 300_001), (4, 200_003), (20, 1 << 20), (2, 70_000)):
+        a = rng.integers(0, sigma, n, dtype=np.uint8)
+        pats = []
+        for m in (1, 2, 3, 5, 8, 17, 40, 64, 200, 1024, 3000):
+            for _ in range(7):
+                s = int(rng.integers(0, n - m + 1))
+                pats.append(a[s:s + m].tobytes())
+        pats.append(bytes([255]) * 9)          # absent symbol (sigma < 256)
+        pats.append(a[:5].tobytes())
+        pats.append(a[n - 7:].tobytes())
+        h = oracle.hist(a)
+        t = dev(a, 3)
+        for lim in (None, n // 3, 1, 0):
+            d = torch.full((len(pats),), -1, dtype=torch.int64, device="cuda")
+            sm.sm_count_batch(pats, t, d, hist=h, max_alignments=lim)
+            got = d.cpu().tolist()
+            for i, p in enumerate(pats):
+                view = a if lim is None else a[: min(n, lim + len(p) - 1)]
+                assert got[i] == oracle.naive_count(p, view), (sigma, n, lim, i, len(p))
+
+
+def test_count_batch_strategies_agree(sm):
+    spec = synth.text_spec("c2", n=(1 << 21) + 5)
+    a = spec.host()
+    t = dev(a, 1)
+    pats = [p.data for p in synth.patterns("c2", spec=spec, per_m=4)]
+    want = [oracle.naive_count(p, a) for p in pats]
+    for strat in (0, 1, 2):
+        d = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
+        sm.sm_count_batch(pats, t, d, strategy=strat)   # hist computed on the device
+        assert d.cpu().tolist() == want, strat
+
+
+def test_count_sharded_virtual(sm):
+    from paper_1612_01506_b200 import dist
+    spec = synth.text_spec("c5", n=(1 << 22) + 77)
+    a = spec.host()
+    t = dev(a)
+    N = a.size
+    h = oracle.hist(a)
+    pats = []
+    for m in (8, 16, 64):
+        for cut in dist.shard_bounds(N, 8)[1:-1]:
+            for s in (cut - 1, cut - m // 2, cut - m + 1, cut):
+                pats.append(a[s:s + m].tobytes())
+    want = [oracle.naive_count(p, a) for p in pats]
+    for G in (1, 2, 8):
+        tot = np.zeros(len(pats), dtype=np.int64)
+        for sh in dist.all_shards(N, G, halo=63):
+            c = dist.count_sharded(pats, t[sh.own_lo: sh.held_hi], sh, hist=h)
+            tot += c.cpu().numpy()
+        assert tot.tolist() == want, G

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--strategy", type=int, default=0)
     ap.add_argument("--peel", type=int, default=0)
     ap.add_argument("--tag", default="")
+    ap.add_argument("--batch", action="store_true", help="time sm_count_batch over the m's patterns")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     spec = synth.text_spec(a.config, n=a.n)
@@ -41,6 +42,20 @@ def main():
            "env": {k: v for k, v in os.environ.items() if k.startswith("SMGPU_")}}
     for m in lengths:
         ps = [p for p in pats if p.m == m]
+        if a.batch:
+            pb = sm.PatternBatch([p.data for p in ps])
+            for _ in range(2):
+                sm.sm_count_batch(pb, t, d, hist=hist, strategy=a.strategy)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(a.reps):
+                sm.sm_count_batch(pb, t, d, hist=hist, strategy=a.strategy)
+            e1.record()
+            torch.cuda.synchronize()
+            us = e0.elapsed_time(e1) * 1e3 / (a.reps * len(ps))
+            res[str(m)] = {"us": round(us, 2), "GBps": round(spec.n / us / 1e3, 1), "host_us": 0}
+            continue
         for _ in range(2):
             for i, p in enumerate(ps):
                 sm.sm_count_async(p.data, t, d[i:i + 1], hist=hist, strategy=a.strategy, peel=a.peel)

@@ -1,0 +1,32 @@
+#!/usr/bin/env python
+"""Read-bandwidth probes on a B200: plain LDG stream vs the TMA staging ring (no compute)."""
+import ctypes, json, os, subprocess, sys
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO = os.path.join(HERE, "libprobe.so")
+if not os.path.exists(SO) or os.path.getmtime(SO) < os.path.getmtime(os.path.join(HERE, "probe.cu")):
+    subprocess.check_call(["nvcc", "-O3", "-shared", "-Xcompiler", "-fPIC", "-gencode", "arch=compute_100a,code=sm_100a",
+                           "-o", SO, os.path.join(HERE, "probe.cu")])
+if __name__ == "__main__":
+    import torch
+    lib = ctypes.CDLL(SO)
+    lib.probe_ldg.restype = ctypes.c_float
+    lib.probe_ldg.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int]
+    lib.probe_tma.restype = ctypes.c_float
+    lib.probe_tma.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                              ctypes.c_uint32, ctypes.c_int, ctypes.c_int]
+    res = {}
+    for n in (1 << 28, 1 << 32):
+        t = torch.empty(n, dtype=torch.uint8, device="cuda")
+        t.fill_(1)
+        p = t.data_ptr()
+        for bps in (2, 4, 8):
+            res[f"ldg n={n>>20}MiB bps={bps}"] = round(lib.probe_ldg(p, n, bps, 10), 1)
+        for tile, stages, ctas, splits in [(32768, 3, 2, 1), (32768, 3, 2, 4), (16384, 6, 2, 1), (16384, 4, 3, 1),
+                                          (8192, 8, 3, 1), (65536, 3, 1, 1), (32768, 6, 1, 1), (16384, 12, 1, 1)]:
+            res[f"tma n={n>>20}MiB tile={tile} st={stages} ctas={ctas} split={splits}"] = round(
+                lib.probe_tma(p, n, tile, stages, ctas, splits, 8, 10), 1)
+        del t
+        torch.cuda.empty_cache()
+    for k, v in res.items():
+        print(f"{k:60s} {v:8.1f} GB/s")
+    print(json.dumps(res))
