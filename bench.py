@@ -349,13 +349,10 @@ def run_native(args):
     if not args.no_report and world == 1:
         tot = int(counts_host.sum())
         posbuf = torch.empty(max(tot, 1), dtype=torch.int64, device=dev)
-        offs = np.concatenate([[0], np.cumsum(counts_host)])
         dcnt = torch.zeros(P, dtype=torch.int64, device=dev)
 
         def rep():
-            for i in range(P):
-                sm.sm_report_async(pdata[i], views[i], posbuf[int(offs[i]): int(offs[i + 1])], dcnt[i:i + 1],
-                                   hist=hh)
+            sm.sm_report_batch(pbatch, held, posbuf, dcnt, hist=hh, max_alignments=shard.owned_bytes)
         rep()
         torch.cuda.synchronize()
         r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -150,6 +150,15 @@ sm_status sm_report_async(const uint8_t* p, size_t m, const uint8_t* t, size_t n
                           int strategy, uint64_t* pos, size_t cap, uint64_t* d_count,
                           void* stream);
 
+/* Enqueue the reporting version for P patterns (see sm_count_batch for p, m,
+ * max_alignments, hist, strategy).  d_counts[i] (DEVICE u64[P]) = count of p[i];
+ * positions of all patterns are written CONCATENATED in pattern order into DEVICE
+ * pos[0..cap): pattern i's ascending positions start at sum_{j<i} d_counts[j].
+ * Positions past cap are dropped (the caller detects truncation from d_counts). */
+sm_status sm_report_batch(const uint8_t* const* p, const size_t* m, size_t P, const uint8_t* t, size_t n,
+                          size_t max_alignments, const uint64_t* hist, int strategy, uint64_t* pos, size_t cap,
+                          uint64_t* d_counts, void* stream);
+
 /* Plan introspection (host-only, no GPU work): the strategy and peeling
  * factor sm_count_async would pick for (p, hist, order).  Used by tests and
  * the benchmark to label measurements. */

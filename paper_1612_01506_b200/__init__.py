@@ -38,7 +38,7 @@ STRATEGY_NAMES = {SM_STRATEGY_FILTER: "filter", SM_STRATEGY_BLOCK: "block"}
 
 EXPORTED_SYMBOLS = (
     "sm_count", "sm_report", "sm_symbol_order", "sm_histogram", "sm_order_from_histogram",
-    "sm_count_async", "sm_count_batch", "sm_report_async", "sm_plan", "sm_last_error", "sm_last_error_message",
+    "sm_count_async", "sm_count_batch", "sm_report_async", "sm_report_batch", "sm_plan", "sm_last_error", "sm_last_error_message",
     "sm_clear_error", "sm_status_string", "sm_version", "sm_launch_count",
 )
 
@@ -81,6 +81,8 @@ def load_library(path: str = LIB_PATH):
     lib.sm_count_async.argtypes = [_u8p, _sz, _u8p, _sz, _vp, _vp, ctypes.c_uint32, ctypes.c_int, _vp, _vp]
     lib.sm_count_batch.restype = ctypes.c_int
     lib.sm_count_batch.argtypes = [_vp, _vp, _sz, _u8p, _sz, _sz, _vp, ctypes.c_int, _vp, _vp]
+    lib.sm_report_batch.restype = ctypes.c_int
+    lib.sm_report_batch.argtypes = [_vp, _vp, _sz, _u8p, _sz, _sz, _vp, ctypes.c_int, _vp, _sz, _vp, _vp]
     lib.sm_report_async.restype = ctypes.c_int
     lib.sm_report_async.argtypes = [_u8p, _sz, _u8p, _sz, _vp, _vp, ctypes.c_uint32, ctypes.c_int, _vp, _sz,
                                     _vp, _vp]
@@ -273,6 +275,23 @@ def sm_count_batch(patterns, t, d_counts, hist=None, max_alignments: Optional[in
     dptr = d_counts if isinstance(d_counts, int) else d_counts.data_ptr()
     s = lib.sm_count_batch(ctypes.addressof(pb.ptrs), ctypes.addressof(pb.lens), pb.P, tp, n, lim, _np_ptr(h),
                            strategy, dptr, _stream(stream))
+    if s != SM_OK:
+        _raise(s)
+
+
+def sm_report_batch(patterns, t, pos, d_counts, hist=None, max_alignments: Optional[int] = None,
+                    strategy: int = SM_STRATEGY_AUTO, stream=None) -> None:
+    """Enqueue reporting for all patterns: d_counts[P] totals, positions concatenated in pattern
+    order into pos (int64 CUDA tensor, capacity pos.numel())."""
+    lib = load_library()
+    pb = patterns if isinstance(patterns, PatternBatch) else PatternBatch(patterns)
+    tp, n = _text(t)
+    h = _u64_host(hist)
+    lim = (1 << 64) - 1 if max_alignments is None else int(max_alignments)
+    cap = 0 if pos is None else pos.numel()
+    pptr = None if pos is None else pos.data_ptr()
+    s = lib.sm_report_batch(ctypes.addressof(pb.ptrs), ctypes.addressof(pb.lens), pb.P, tp, n, lim, _np_ptr(h),
+                            strategy, pptr, cap, d_counts.data_ptr(), _stream(stream))
     if s != SM_OK:
         _raise(s)
 

@@ -207,10 +207,9 @@ sm_status host_hist(const uint8_t* t, size_t n, cudaStream_t st, uint64_t* out) 
 
 // Descriptor of one planned pattern (see search.cuh).  `lim` = max alignments to
 // count (SIZE_MAX: all n - m + 1).
-void fill_desc(const Plan& pl, const uint8_t* p, size_t m, uint64_t delta, uint64_t n, uint64_t lim, PatDesc& d,
-               uint32_t tbl_index) {
+void fill_desc(const Plan& pl, const uint8_t* p, size_t m, uint64_t delta, uint64_t n, uint64_t lim, uint64_t T,
+               PatDesc& d, uint32_t tbl_index) {
   std::memset(&d, 0, sizeof(d));
-  const uint64_t T = pl.tile;
   d.m = (uint32_t)m;
   d.r = pl.r;
   d.tbl = tbl_index;
@@ -253,7 +252,9 @@ struct Planned {
   uint64_t* count_out;
 };
 
-// Build one launch over patterns `ps` (same strategy, same tile; <= kMaxBatch, table <= kTableLarge).
+// Build one launch over patterns `ps` (same strategy; <= kMaxBatch, table <= kTableLarge).
+// The tile starts at the plan's (large texts: 32 KiB) and is halved while fewer than
+// 3 ring stages fit in a CTA's shared memory (long patterns carry ~m bytes of halo).
 void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_t n, uint64_t lim, int epilogue,
                   HostLaunch& L) {
   const uintptr_t tp = reinterpret_cast<uintptr_t>(t);
@@ -261,42 +262,52 @@ void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_
   L.a.base = reinterpret_cast<const uint8_t*>(tp & ~(uintptr_t)15);
   L.a.delta = tp & 15;
   L.a.n = n;
-  L.a.tile = ps[0]->pl.tile;
   L.strategy = ps[0]->pl.strategy;
-  L.cpl = ps[0]->pl.cpl;
   L.epilogue = epilogue;
-  L.d.resize(ps.size());
   L.e.clear();
-  uint64_t work = 0;
-  uint32_t max_stage = 0;
-  for (size_t i = 0; i < ps.size(); ++i) {
-    const Planned& q = *ps[i];
-    fill_desc(q.pl, q.p, q.m, L.a.delta, n, lim, L.d[i], (uint32_t)L.e.size());
-    for (size_t k = 0; k < q.m; ++k) L.e.push_back(q.pl.order[k] | ((uint32_t)q.p[q.pl.order[k]] << 16));
-    work += L.d[i].ntiles;
-    L.d[i].work_end = work;
-    L.d[i].count_out = q.count_out;
-    max_stage = std::max(max_stage, L.d[i].stage_len);
-  }
+  for (const Planned* q : ps)
+    for (size_t k = 0; k < q->m; ++k) L.e.push_back(q->pl.order[k] | ((uint32_t)q->p[q->pl.order[k]] << 16));
   L.a.npat = (uint32_t)ps.size();
-  L.a.total_work = work;
   L.a.tbl_words = (uint32_t)L.e.size();
-  L.a.stage_stride = (max_stage + 127) & ~127u;
   L.a.ring_off = (kTblOff + 4 * L.a.tbl_words + 127) & ~127u;
-  // shared memory per SM: 228 KiB, 1 KiB reserved per resident CTA
-  int ctas = tunables().ctas_per_sm;
-  uint32_t stages = 0;
-  for (; ctas >= 1; --ctas) {
-    const uint32_t budget = std::min<uint32_t>(227 * 1024, 233472 / ctas - 1024);
-    stages = budget > L.a.ring_off ? (budget - L.a.ring_off) / L.a.stage_stride : 0;
-    if (stages >= 2) break;
+  uint32_t T = ps[0]->pl.tile;
+  for (;;) {
+    L.a.tile = T;
+    L.cpl = (int)(T / (16u * kLanesPerTilePass));
+    L.d.resize(ps.size());
+    uint64_t work = 0;
+    uint32_t max_stage = 0, tbl = 0;
+    for (size_t i = 0; i < ps.size(); ++i) {
+      const Planned& q = *ps[i];
+      fill_desc(q.pl, q.p, q.m, L.a.delta, n, lim, T, L.d[i], tbl);
+      tbl += (uint32_t)q.m;
+      work += L.d[i].ntiles;
+      L.d[i].work_end = work;
+      L.d[i].count_out = q.count_out;
+      max_stage = std::max(max_stage, L.d[i].stage_len);
+    }
+    L.a.total_work = work;
+    L.a.stage_stride = (max_stage + 127) & ~127u;
+    // shared memory per SM: 228 KiB, 1 KiB reserved per resident CTA
+    int ctas = tunables().ctas_per_sm;
+    uint32_t stages = 0;
+    for (; ctas >= 1; --ctas) {
+      const uint32_t budget = std::min<uint32_t>(227 * 1024, 233472 / ctas - 1024);
+      stages = budget > L.a.ring_off ? (budget - L.a.ring_off) / L.a.stage_stride : 0;
+      if (stages >= 2) break;
+    }
+    if (ctas < 1) ctas = 1;
+    if (stages < 3 && T > 4096) {
+      T /= 2;
+      continue;
+    }
+    L.a.stages = std::min<uint32_t>(stages, tunables().max_stages);
+    L.smem = (size_t)L.a.ring_off + (size_t)L.a.stages * L.a.stage_stride;
+    const uint64_t sms = (uint64_t)num_sms();
+    L.grid = (int)std::min<uint64_t>(work, sms * (uint64_t)ctas);
+    if (L.grid < 1) L.grid = 1;
+    return;
   }
-  if (ctas < 1) ctas = 1;
-  L.a.stages = std::min<uint32_t>(stages, tunables().max_stages);
-  L.smem = (size_t)L.a.ring_off + (size_t)L.a.stages * L.a.stage_stride;
-  const uint64_t sms = (uint64_t)num_sms();
-  L.grid = (int)std::min<uint64_t>(work, sms * (uint64_t)ctas);
-  if (L.grid < 1) L.grid = 1;
 }
 
 sm_status prepare(const uint8_t* p, size_t m, const uint8_t* t, size_t n, const uint64_t* hist,
@@ -380,21 +391,56 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
   return SM_OK;
 }
 
-sm_status enqueue_report(const uint8_t* p, size_t m, const uint8_t* t, size_t n, const uint64_t* hist,
-                         const uint32_t* order, uint32_t peel, int strategy, uint64_t* pos, size_t cap,
-                         uint64_t* d_count, cudaStream_t st) {
-  SM_CUDA_TRY(cudaMemsetAsync(d_count, 0, sizeof(uint64_t), st), "cudaMemsetAsync(count)");
-  if (n < m) return SM_OK;
-  Planned q{Plan(), p, m, nullptr};
+// Reporting (A8) for P patterns, output concatenated in pattern order: pattern k's
+// ascending positions at pos[off_k ..), off_k = sum of earlier counts (first `cap`
+// positions overall are written).  Pass 1: per-(pattern, tile) counts and per-pattern
+// totals; one exclusive scan over all work items; pass 2 writes, visiting only
+// tiles with matches.  Launches cover consecutive runs of the caller's patterns.
+sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_t P, const uint8_t* t, size_t n,
+                               uint64_t lim, const uint64_t* hist, const uint32_t* order, uint32_t peel,
+                               int strategy, uint64_t* pos, size_t cap, uint64_t* d_counts, cudaStream_t st) {
+  if (P == 0) return SM_OK;
+  SM_CUDA_TRY(cudaMemsetAsync(d_counts, 0, P * sizeof(uint64_t), st), "cudaMemsetAsync(counts)");
   uint64_t hb[256];
-  sm_status s = prepare(p, m, t, n, hist, order, peel, strategy, st, q.pl, hb);
-  if (s != SM_OK) return s;
-  HostLaunch L;
-  build_launch({&q}, t, n, UINT64_MAX, kEpiTileCount, L);
-
-  // scratch: per-tile counts (ntiles + 1, last = 0) and their exclusive prefix
-  const uint64_t ntiles = L.d[0].ntiles;
-  const uint64_t nt1 = ntiles + 1;
+  const uint64_t* h = hist;
+  if (!h) {
+    sm_status s = host_hist(t, n, st, hb);
+    if (s != SM_OK) return s;
+    h = hb;
+  }
+  std::vector<Planned> plans;
+  plans.reserve(P);
+  for (size_t i = 0; i < P; ++i) {
+    if (n < ms[i] || lim == 0) continue;  // no alignments: count 0, no positions
+    Planned q{Plan(), ps[i], ms[i], d_counts + i};
+    sm_status s = make_plan(ps[i], ms[i], n, h, P == 1 ? order : nullptr, P == 1 ? peel : 0, strategy, q.pl);
+    if (s != SM_OK) return s;
+    plans.push_back(std::move(q));
+  }
+  if (plans.empty()) return SM_OK;
+  // launches over consecutive runs (same strategy, batch limits), in pattern order
+  std::vector<HostLaunch> Ls;
+  {
+    std::vector<const Planned*> run;
+    size_t words = 0;
+    for (size_t i = 0; i <= plans.size(); ++i) {
+      const bool end = i == plans.size();
+      if (!run.empty() && (end || plans[i].pl.strategy != run[0]->pl.strategy || run.size() == (size_t)kMaxBatch ||
+                           words + plans[i].m > (size_t)kTableLarge)) {
+        Ls.emplace_back();
+        build_launch(run, t, n, lim, kEpiTileCount, Ls.back());
+        run.clear();
+        words = 0;
+      }
+      if (!end) {
+        run.push_back(&plans[i]);
+        words += plans[i].m;
+      }
+    }
+  }
+  uint64_t total_work = 0;
+  for (const HostLaunch& L : Ls) total_work += L.a.total_work;
+  const uint64_t nt1 = total_work + 1;
   size_t temp_bytes = 0;
   SM_CUDA_TRY(exclusive_scan_u64(nullptr, nullptr, nt1, nullptr, &temp_bytes, st), "scan sizing");
   const size_t off_bytes = ((nt1 * 8 + 255) / 256) * 256;
@@ -405,28 +451,43 @@ sm_status enqueue_report(const uint8_t* p, size_t m, const uint8_t* t, size_t n,
   uint64_t* offsets = reinterpret_cast<uint64_t*>(scratch + off_bytes);
   void* temp = scratch + 2 * off_bytes;
   cudaError_t e = cudaMemsetAsync(counts, 0, nt1 * 8, st);
-  if (e == cudaSuccess) {
-    L.a.tile_counts = counts;
-    e = launch_search(L, st);  // pass 1: per-tile counts
+  uint64_t wb = 0;
+  for (HostLaunch& L : Ls) {  // pass 1
+    if (e != cudaSuccess) break;
+    L.a.tile_counts = counts + wb;
+    e = launch_search(L, st);
     if (e == cudaSuccess) ++g_launches;
+    wb += L.a.total_work;
   }
   if (e == cudaSuccess) {
     e = exclusive_scan_u64(counts, offsets, nt1, temp, &temp_bytes, st);
     if (e == cudaSuccess) g_launches += 1;
   }
-  if (e == cudaSuccess) e = cudaMemcpyAsync(d_count, offsets + ntiles, 8, cudaMemcpyDeviceToDevice, st);
-  if (e == cudaSuccess && cap > 0) {
-    L.epilogue = kEpiWrite;
-    L.a.tile_counts = nullptr;
-    L.a.tile_offsets = offsets;
-    L.a.pos = pos;
-    L.a.cap = cap;
-    e = launch_search(L, st);  // pass 2: ranked writes in tiles with matches
-    if (e == cudaSuccess) ++g_launches;
+  wb = 0;
+  if (cap > 0) {
+    for (HostLaunch& L : Ls) {  // pass 2
+      if (e != cudaSuccess) break;
+      L.epilogue = kEpiWrite;
+      L.a.tile_counts = nullptr;
+      L.a.tile_offsets = offsets + wb;
+      L.a.pos = pos;
+      L.a.cap = cap;
+      e = launch_search(L, st);
+      if (e == cudaSuccess) ++g_launches;
+      wb += L.a.total_work;
+    }
   }
   cudaFreeAsync(scratch, st);
   if (e != cudaSuccess) return cuda_fail(e, "report");
   return SM_OK;
+}
+
+sm_status enqueue_report(const uint8_t* p, size_t m, const uint8_t* t, size_t n, const uint64_t* hist,
+                         const uint32_t* order, uint32_t peel, int strategy, uint64_t* pos, size_t cap,
+                         uint64_t* d_count, cudaStream_t st) {
+  const uint8_t* ps[1] = {p};
+  const size_t ms[1] = {m};
+  return enqueue_report_batch(ps, ms, 1, t, n, UINT64_MAX, hist, order, peel, strategy, pos, cap, d_count, st);
 }
 
 }  // namespace
@@ -554,6 +615,33 @@ sm_status sm_count_batch(const uint8_t* const* p, const size_t* m, size_t P, con
   sm_status s = check_device_ptr(d_counts, "d_counts");
   if (s != SM_OK) return s;
   return enqueue_count_batch(p, m, P, t, n, (uint64_t)max_alignments, hist, strategy, d_counts, as_stream(stream));
+}
+
+sm_status sm_report_batch(const uint8_t* const* p, const size_t* m, size_t P, const uint8_t* t, size_t n,
+                          size_t max_alignments, const uint64_t* hist, int strategy, uint64_t* pos, size_t cap,
+                          uint64_t* d_counts, void* stream) {
+  if (P == 0) return SM_OK;
+  if (!p || !m || !d_counts) return fail(SM_EINVAL, "NULL argument");
+  if (strategy < SM_STRATEGY_AUTO || strategy > SM_STRATEGY_BLOCK) return fail(SM_EINVAL, "bad strategy");
+  for (size_t i = 0; i < P; ++i) {
+    if (m[i] == 0) return fail(SM_EINVAL, "m[i] == 0: empty pattern is undefined (reading R2)");
+    if (m[i] > SM_MAX_PATTERN) return fail(SM_EINVAL, "m[i] > SM_MAX_PATTERN (4096)");
+    if (!p[i]) return fail(SM_EINVAL, "p[i] is NULL");
+  }
+  if (n > 0) {
+    if (!t) return fail(SM_EINVAL, "t is NULL with n > 0");
+    sm_status s = check_device_ptr(t, "t");
+    if (s != SM_OK) return s;
+  }
+  sm_status s = check_device_ptr(d_counts, "d_counts");
+  if (s != SM_OK) return s;
+  if (cap > 0) {
+    if (!pos) return fail(SM_EINVAL, "pos is NULL with cap > 0");
+    s = check_device_ptr(pos, "pos");
+    if (s != SM_OK) return s;
+  }
+  return enqueue_report_batch(p, m, P, t, n, (uint64_t)max_alignments, hist, nullptr, 0, strategy, pos, cap,
+                              d_counts, as_stream(stream));
 }
 
 sm_status sm_report_async(const uint8_t* p, size_t m, const uint8_t* t, size_t n, const uint64_t* hist,

@@ -37,7 +37,7 @@ struct PatDesc {
   uint64_t work_end;   // this pattern's work items are [work_end - ntiles, work_end)
   uint64_t edge_lo;    // tiles ti < edge_lo start before the first alignment
   uint64_t edge_hi;    // tiles ti >= edge_hi end after the last alignment
-  uint64_t* count_out; // kEpiCount: device u64 (accumulated with atomics; zeroed by host)
+  uint64_t* count_out; // kEpiCount / kEpiTileCount: device u64 (accumulated with atomics; zeroed by host)
   uint32_t m;
   uint32_t r;          // peeling factor (BLOCK), 1 <= r <= m
   uint32_t a1;         // pattern offset of pi(1) (FILTER)
@@ -59,10 +59,10 @@ struct LaunchArgs {
   uint32_t stage_stride;     // smem stride between stages (multiple of 128)
   uint32_t stages;           // ring depth
   uint32_t ring_off;         // smem byte offset of stage 0
-  uint32_t npat;             // patterns in the batch (1 for the report epilogues)
+  uint32_t npat;             // patterns in the batch
   uint32_t tbl_words;        // table entries
-  uint64_t* tile_counts;     // kEpiTileCount: u64[ntiles] (zeroed by host)
-  const uint64_t* tile_offsets;  // kEpiWrite: exclusive prefix, ntiles + 1 entries
+  uint64_t* tile_counts;     // kEpiTileCount: u64[total_work] per work item (zeroed by host)
+  const uint64_t* tile_offsets;  // kEpiWrite: exclusive prefix over work items, total_work + 1 entries
   uint64_t* pos;             // kEpiWrite: output positions
   uint64_t cap;              // kEpiWrite: capacity of pos
 };

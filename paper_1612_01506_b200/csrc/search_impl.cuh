@@ -140,7 +140,7 @@ __device__ void produce(const LaunchParams<CAP>& P, uint8_t* ring, uint64_t* ful
     while (w >= P.d[k].work_end) ++k;
     const PatDesc& d = P.d[k];
     const uint64_t ti = w - (d.work_end - d.ntiles);
-    if (EPI == kEpiWrite && a.tile_offsets[ti + 1] == a.tile_offsets[ti]) continue;
+    if (EPI == kEpiWrite && a.tile_offsets[w + 1] == a.tile_offsets[w]) continue;
     if (wrapped) mbar_wait_sleep(&empty[s], ph ^ 1u);  // consumers released this stage's previous use
     uint8_t* buf = ring + (size_t)s * a.stage_stride;
     const int64_t lo = (int64_t)((d.k_begin + ti) * a.tile) - (int64_t)d.pre;
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
     }
     const PatDesc& d = P.d[k];
     const uint64_t ti = w - (d.work_end - d.ntiles);
-    if (EPI == kEpiWrite && a.tile_offsets[ti + 1] == a.tile_offsets[ti]) continue;
+    if (EPI == kEpiWrite && a.tile_offsets[w + 1] == a.tile_offsets[w]) continue;
     mbar_wait(&full[s], ph);
     const uint8_t* buf = ring + (size_t)s * a.stage_stride;
     const Pat pt{d.m, d.r, d.a1, d.bc1, d.s2, d.bc2, d.pre, tbl + d.tbl};
@@ -425,8 +425,10 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
           acc += cs.n;
         } else {
           const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, cs.n);
-          if (lane == 0 && ws)
-            atomicAdd(reinterpret_cast<unsigned long long*>(&a.tile_counts[ti]), (unsigned long long)ws);
+          if (lane == 0 && ws) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(&a.tile_counts[w]), (unsigned long long)ws);
+            atomicAdd(reinterpret_cast<unsigned long long*>(d.count_out), (unsigned long long)ws);
+          }
         }
       } else {  // two passes: this warp's total, then ranked writes
         CountSink cs;
@@ -434,7 +436,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
         const uint32_t wtot = __reduce_add_sync(0xFFFFFFFFu, cs.n);
         if (lane == 0) s_wt[par * kConsumerWarps + warp] = wtot;
         named_bar_sync(1, kConsumerWarps * 32);
-        WriteSink ws{a.tile_offsets[ti], x_base - (int64_t)a.delta, a.pos, a.cap};
+        WriteSink ws{a.tile_offsets[w], x_base - (int64_t)a.delta, a.pos, a.cap};
         for (int wv = 0; wv < warp; ++wv) ws.run += s_wt[par * kConsumerWarps + wv];
         filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, ws);
         par ^= 1u;
@@ -449,13 +451,15 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
         acc += tc;
       } else if (EPI == kEpiTileCount) {
         const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, tc);
-        if (lane == 0 && ws)
-          atomicAdd(reinterpret_cast<unsigned long long*>(&a.tile_counts[ti]), (unsigned long long)ws);
+        if (lane == 0 && ws) {
+          atomicAdd(reinterpret_cast<unsigned long long*>(&a.tile_counts[w]), (unsigned long long)ws);
+          atomicAdd(reinterpret_cast<unsigned long long*>(d.count_out), (unsigned long long)ws);
+        }
       } else {
         const uint32_t wtot = __reduce_add_sync(0xFFFFFFFFu, tc);
         if (lane == 0) s_wt[par * kConsumerWarps + warp] = wtot;
         named_bar_sync(1, kConsumerWarps * 32);
-        WriteSink ws{a.tile_offsets[ti], x_base - (int64_t)a.delta, a.pos, a.cap};
+        WriteSink ws{a.tile_offsets[w], x_base - (int64_t)a.delta, a.pos, a.cap};
         for (int wv = 0; wv < warp; ++wv) ws.run += s_wt[par * kConsumerWarps + wv];
 #pragma unroll
         for (int it = 0; it < CPL; ++it) ws(cw0 + it * 32u + lane, g[it], lane);

@@ -313,3 +313,24 @@ def test_count_sharded_virtual(sm):
             c = dist.count_sharded(pats, t[sh.own_lo: sh.held_hi], sh, hist=h)
             tot += c.cpu().numpy()
         assert tot.tolist() == want, G
+
+
+def test_report_batch_concatenated(sm):
+    rng = np.random.default_rng(5150)
+    for sigma, n in ((2, 100_001), (96, 400_003), (4, 1 << 20)):
+        a = rng.integers(0, sigma, n, dtype=np.uint8)
+        pats = []
+        for m in (1, 2, 3, 7, 16, 40, 300):
+            for _ in range(6):
+                s = int(rng.integers(0, n - m + 1))
+                pats.append(a[s:s + m].tobytes())
+        t = dev(a, 7)
+        want_pos = [oracle.naive_report(p, a) for p in pats]
+        want_cnt = [w.size for w in want_pos]
+        flat = np.concatenate(want_pos) if want_pos else np.zeros(0, np.uint64)
+        for cap in (flat.size, flat.size // 3, 0):
+            d = torch.full((len(pats),), -1, dtype=torch.int64, device="cuda")
+            pos = torch.full((max(cap, 1),), -7, dtype=torch.int64, device="cuda")
+            sm.sm_report_batch(pats, t, pos[:cap] if cap else None, d, hist=oracle.hist(a))
+            assert d.cpu().tolist() == want_cnt
+            assert pos[:cap].cpu().numpy().astype(np.uint64).tolist() == flat[:cap].tolist(), (sigma, cap)
