@@ -253,8 +253,8 @@ struct Planned {
 };
 
 // Build one launch over patterns `ps` (same strategy; <= kMaxBatch, table <= kTableLarge).
-// The tile starts at the plan's (large texts: 32 KiB) and is halved while fewer than
-// 3 ring stages fit in a CTA's shared memory (long patterns carry ~m bytes of halo).
+// The tile is the plan's (large texts: 32 KiB); the batching loops keep a launch's
+// table <= kBatchTableWords so that 3 stages fit; T is halved only if fewer than 2 do.
 void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_t n, uint64_t lim, int epilogue,
                   HostLaunch& L) {
   const uintptr_t tp = reinterpret_cast<uintptr_t>(t);
@@ -297,7 +297,7 @@ void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_
       if (stages >= 2) break;
     }
     if (ctas < 1) ctas = 1;
-    if (stages < 3 && T > 4096) {
+    if (stages < 2 && T > 4096) {  // only a single very long pattern can get here
       T /= 2;
       continue;
     }
@@ -378,7 +378,7 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
     };
     for (const Planned& q : plans) {
       if (q.pl.strategy != strat) continue;
-      if (batch.size() == (size_t)kMaxBatch || words + q.m > (size_t)kTableLarge) {
+      if (batch.size() == (size_t)kMaxBatch || words + q.m > (size_t)kBatchTableWords) {
         sm_status s = flush();
         if (s != SM_OK) return s;
       }
@@ -426,7 +426,7 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
     for (size_t i = 0; i <= plans.size(); ++i) {
       const bool end = i == plans.size();
       if (!run.empty() && (end || plans[i].pl.strategy != run[0]->pl.strategy || run.size() == (size_t)kMaxBatch ||
-                           words + plans[i].m > (size_t)kTableLarge)) {
+                           words + plans[i].m > (size_t)kBatchTableWords)) {
         Ls.emplace_back();
         build_launch(run, t, n, lim, kEpiTileCount, Ls.back());
         run.clear();
