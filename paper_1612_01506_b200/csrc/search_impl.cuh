@@ -73,6 +73,17 @@ __device__ __forceinline__ uint4 load_window16(const uint8_t* base16, uint32_t s
   return w;
 }
 
+// Same window with the word offset Q = (sel >> 2) & 3 fixed at compile time (callers
+// branch once per warp-uniform step, not once per chunk); sh = 8 * (sel & 3).
+template <int Q>
+__device__ __forceinline__ uint4 window16_q(const uint8_t* base16, uint32_t sh) {
+  const uint4 lo = lds128(base16);
+  const uint4 hi = lds128(base16 + 16);
+  const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+  return make_uint4(byte_window(w[Q], w[Q + 1], sh), byte_window(w[Q + 1], w[Q + 2], sh),
+                    byte_window(w[Q + 2], w[Q + 3], sh), byte_window(w[Q + 3], w[Q + 4], sh));
+}
+
 // found &= SIMDcompare(...) for the 16 alignments whose compared bytes are `w`
 __device__ __forceinline__ void found_and_eq(Found4& F, const uint4 w, uint32_t bc) {
   F.f0 &= eq_flags_raw(w.x, bc);
@@ -199,11 +210,14 @@ __device__ __forceinline__ uint32_t g_to_mask16(uint32_t g) {
 // 16 alignments -- exact packed-byte compares of pi(1) and pi(2) without a test
 // in between.  Returns the compressed found word (bit
 // (8k + 7 - i) <-> tile-relative alignment u = 16c + 4i + k) of the survivors.
+// Q = word offset of pi(2)'s window (warp-uniform per pattern, compile time).
+template <int Q>
 __device__ __forceinline__ uint32_t filter_entry(const Pat& pt, const uint8_t* buf, uint32_t c, bool edge,
                                                  int32_t rlo, int32_t rhi) {
   Found4 F = edge ? found_from_mask16(range_mask16_rel((int32_t)(16u * c), rlo, rhi)) : found_all();
-  found_and_eq(F, lds128(buf + pt.pre + 16u * c), pt.bc1);                                        // pi(1)
-  if (pt.m >= 2) found_and_eq(F, load_window16(buf + 16u * c + (pt.s2 & ~15u), pt.s2), pt.bc2);  // pi(2)
+  found_and_eq(F, lds128(buf + pt.pre + 16u * c), pt.bc1);  // pi(1)
+  if (pt.m >= 2)                                               // pi(2)
+    found_and_eq(F, window16_q<Q>(buf + 16u * c + (pt.s2 & ~15u), (pt.s2 & 3u) * 8u), pt.bc2);
   return compress_found(F);
 }
 
@@ -287,10 +301,26 @@ struct CountSink {
   __device__ __forceinline__ void operator()(uint32_t, uint32_t g, int) { n += __popc(g); }
 };
 
+// Phase B of a FILTER tile: drain the warp's queue 32 entries at a time, one chunk
+// per lane, all lanes busy.
+template <int Q, class Sink>
+__device__ __forceinline__ void filter_drain(const Pat& pt, const uint8_t* buf, int lane, const uint16_t* qc,
+                                             uint32_t qlen, bool edge, int32_t rlo, int32_t rhi, Sink& sink) {
+  for (uint32_t b0 = 0; b0 < qlen; b0 += 32) {
+    const uint32_t i = b0 + lane;
+    uint32_t c = 0, g = 0;
+    if (i < qlen) {
+      c = qc[i];
+      g = filter_entry<Q>(pt, buf, c, edge, rlo, rhi);
+    }
+    if (pt.m >= 3) g = verify_survivors(pt, buf, c, g, lane);
+    sink(c, g, lane);
+  }
+}
+
 // One warp's share of a FILTER tile, in groups of kGroup chunk-rows: phase A
 // ballot-compacts the chunks whose pi(1)-bytes contain p[pi(1)] into the warp's
-// queue (ascending chunk order); phase B drains it 32 entries at a time, one
-// chunk per lane, all lanes busy.
+// queue (ascending chunk order); phase B (filter_drain) verifies them.
 template <int CPL, class Sink>
 __device__ __forceinline__ void filter_tile(const Pat& pt, const uint8_t* buf, uint32_t cw0, int lane, uint16_t* qc,
                                             bool edge, int32_t rlo, int32_t rhi, Sink& sink) {
@@ -307,17 +337,33 @@ __device__ __forceinline__ void filter_tile(const Pat& pt, const uint8_t* buf, u
       qlen += __popc(bal);
     }
     __syncwarp();
-    for (uint32_t b0 = 0; b0 < qlen; b0 += 32) {
-      const uint32_t i = b0 + lane;
-      uint32_t c = 0, g = 0;
-      if (i < qlen) {
-        c = qc[i];
-        g = filter_entry(pt, buf, c, edge, rlo, rhi);
-      }
-      if (pt.m >= 3) g = verify_survivors(pt, buf, c, g, lane);
-      sink(c, g, lane);
+    switch ((pt.s2 >> 2) & 3u) {  // warp-uniform
+      case 0: filter_drain<0>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink); break;
+      case 1: filter_drain<1>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink); break;
+      case 2: filter_drain<2>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink); break;
+      default: filter_drain<3>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink); break;
     }
     __syncwarp();
+  }
+}
+
+// One BLOCK step (pattern offset off, broadcast symbol bc) over the CPL chunks of a lane.
+template <int CPL, int Q>
+__device__ __forceinline__ void block_step_q(Found4 (&F)[CPL], const uint8_t* cbase, uint32_t off, uint32_t bc) {
+  const uint32_t sh = (off & 3u) * 8u;
+  const uint8_t* b = cbase + (off & ~15u);
+#pragma unroll
+  for (int it = 0; it < CPL; ++it) found_and_eq(F[it], window16_q<Q>(b + it * 512u, sh), bc);
+}
+
+template <int CPL>
+__device__ __forceinline__ void block_step(Found4 (&F)[CPL], const uint8_t* cbase, uint32_t e) {
+  const uint32_t off = e & 0xFFFFu, bc = (e >> 16) * 0x01010101u;
+  switch ((off >> 2) & 3u) {  // warp-uniform
+    case 0: block_step_q<CPL, 0>(F, cbase, off, bc); break;
+    case 1: block_step_q<CPL, 1>(F, cbase, off, bc); break;
+    case 2: block_step_q<CPL, 2>(F, cbase, off, bc); break;
+    default: block_step_q<CPL, 3>(F, cbase, off, bc); break;
   }
 }
 
@@ -330,24 +376,15 @@ __device__ __forceinline__ void block_tile(const Pat& pt, const uint8_t* buf, ui
   for (int it = 0; it < CPL; ++it)
     F[it] = edge ? found_from_mask16(range_mask16_rel((int32_t)(16u * (cw0 + it * 32u + lane)), rlo, rhi))
                  : found_all();
+  const uint8_t* cbase = buf + 16u * (cw0 + lane);  // chunk it of this lane is at cbase + 512 * it
   uint32_t k = 0;
-  for (; k < pt.r; ++k) {  // peeled: all r comparisons, no test
-    const uint32_t e = pt.tbl[k];
-    const uint32_t off = e & 0xFFFFu, bc = (e >> 16) * 0x01010101u;
-#pragma unroll
-    for (int it = 0; it < CPL; ++it)
-      found_and_eq(F[it], load_window16(buf + 16u * (cw0 + it * 32u + lane) + (off & ~15u), off), bc);
-  }
+  for (; k < pt.r; ++k) block_step<CPL>(F, cbase, pt.tbl[k]);  // peeled: all r, no test
   for (; k < pt.m; ++k) {  // ordered loop with exit test, warp-uniform
     uint32_t any = 0;
 #pragma unroll
     for (int it = 0; it < CPL; ++it) any |= found_any(F[it]);
     if (!__any_sync(0xFFFFFFFFu, any != 0)) break;
-    const uint32_t e = pt.tbl[k];
-    const uint32_t off = e & 0xFFFFu, bc = (e >> 16) * 0x01010101u;
-#pragma unroll
-    for (int it = 0; it < CPL; ++it)
-      found_and_eq(F[it], load_window16(buf + 16u * (cw0 + it * 32u + lane) + (off & ~15u), off), bc);
+    block_step<CPL>(F, cbase, pt.tbl[k]);
   }
 #pragma unroll
   for (int it = 0; it < CPL; ++it) g_out[it] = compress_found(F[it]);  // popcount of found
