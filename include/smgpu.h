@@ -72,11 +72,17 @@ typedef enum sm_status {
  *     16 alignments per lane, then the pi-ordered loop over the warp's 512
  *     alignments with a warp-uniform exit test.  Best for
  *     small alphabets / periodic text.
+ *  SM_STRATEGY_PACKED: BLOCK on b-bit codes (b = 1 or 2) of the text bytes,
+ *     code(x) = (x >> s) & (2^b - 1) with s chosen so that the code is injective
+ *     on the symbols present in t (from hist: it MUST be t's histogram); needs
+ *     <= 4 text symbols and every pattern symbol present in t, else SM_EINVAL.
+ *     For DNA / binary text (compare-bound regime).
  *  SM_STRATEGY_AUTO: chosen on the host from the text histogram. */
 typedef enum sm_strategy {
   SM_STRATEGY_AUTO = 0,
   SM_STRATEGY_FILTER = 1,
-  SM_STRATEGY_BLOCK = 2
+  SM_STRATEGY_BLOCK = 2,
+  SM_STRATEGY_PACKED = 3
 } sm_strategy;
 
 #define SM_COUNT_ERROR UINT64_MAX

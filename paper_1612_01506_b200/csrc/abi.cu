@@ -119,6 +119,7 @@ struct Tunables {
   int ctas_per_sm = 2;          // persistent CTAs per SM
   uint32_t max_stages = 8;      // ring depth cap per CTA
   double filter_max_f = 0;      // AUTO: override of the FILTER threshold on f(pi(1)) (0 = built-in)
+  bool auto_packed = true;      // AUTO may pick PACKED for small text alphabets
 };
 
 const Tunables& tunables() {
@@ -128,6 +129,7 @@ const Tunables& tunables() {
     if (const char* e = std::getenv("SMGPU_CTAS_PER_SM")) x.ctas_per_sm = std::atoi(e);
     if (const char* e = std::getenv("SMGPU_STAGES")) x.max_stages = (uint32_t)std::atoi(e);
     if (const char* e = std::getenv("SMGPU_FILTER_MAX_F")) x.filter_max_f = std::atof(e);
+    if (const char* e = std::getenv("SMGPU_AUTO_PACKED")) x.auto_packed = std::atoi(e) != 0;
     if (x.tile != 4096 && x.tile != 8192 && x.tile != 16384 && x.tile != 32768) x.tile = 32768;
     if (x.ctas_per_sm < 1 || x.ctas_per_sm > 3) x.ctas_per_sm = 2;
     if (x.max_stages < 2 || x.max_stages > (uint32_t)kMaxStages) x.max_stages = kMaxStages;
@@ -138,6 +140,7 @@ const Tunables& tunables() {
 
 struct Plan {
   int strategy = kFilter;
+  uint32_t code_shift = 0;  // PACKED: code field shift
   uint32_t r = 1;
   int cpl = 4;
   uint32_t tile = 16384;
@@ -153,9 +156,37 @@ void choose_tiling(uint64_t n, Plan& pl) {
   pl.cpl = (int)(pl.tile / (16u * kLanesPerTilePass));
 }
 
+// PACKED applicability: a b-bit field (x >> s) & (2^b - 1), b in {1, 2}, that is
+// injective on the symbols present in t, and every pattern symbol present in t.
+// Returns the strategy (kPacked1 / kPacked2) or 0; *shift receives s.
+int packed_projection(const uint64_t* hist, const uint8_t* p, size_t m, uint32_t* shift) {
+  int present = 0;
+  for (int c = 0; c < 256; ++c) present += hist[c] > 0;
+  for (size_t j = 0; j < m; ++j)
+    if (hist[p[j]] == 0) return 0;  // an absent symbol: FILTER answers 0 at once
+  for (int b = 1; b <= 2; ++b) {
+    if (present > (1 << b)) continue;
+    for (uint32_t s = 0; s + b <= 8; ++s) {
+      bool used[4] = {false, false, false, false};
+      bool ok = true;
+      for (int c = 0; c < 256 && ok; ++c) {
+        if (!hist[c]) continue;
+        const uint32_t code = ((uint32_t)c >> s) & ((1u << b) - 1u);
+        if (used[code]) ok = false;
+        used[code] = true;
+      }
+      if (ok) {
+        *shift = s;
+        return b == 1 ? kPacked1 : kPacked2;
+      }
+    }
+  }
+  return 0;
+}
+
 sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist, const uint32_t* order,
                     uint32_t peel, int strategy, Plan& pl) {
-  if (strategy < SM_STRATEGY_AUTO || strategy > SM_STRATEGY_BLOCK) return fail(SM_EINVAL, "bad strategy");
+  if (strategy < SM_STRATEGY_AUTO || strategy > SM_STRATEGY_PACKED) return fail(SM_EINVAL, "bad strategy");
   pl.order.resize(m);
   if (order) {
     if (!valid_permutation(order, m)) return fail(SM_EINVAL, "order is not a permutation of 0..m-1");
@@ -175,6 +206,15 @@ sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist
     const double f1 = freq(0);
     const double thr = tunables().filter_max_f > 0 ? tunables().filter_max_f : (m <= 2 ? 0.035 : 0.06);
     strategy = f1 <= thr ? kFilter : kBlock;
+    if (strategy == kBlock && tunables().auto_packed) {  // small text alphabet: compare b-bit codes
+      const int pk = packed_projection(hist, p, m, &pl.code_shift);
+      if (pk) strategy = pk;
+    }
+  } else if (strategy == SM_STRATEGY_PACKED) {
+    strategy = packed_projection(hist, p, m, &pl.code_shift);
+    if (!strategy)
+      return fail(SM_EINVAL, "SM_STRATEGY_PACKED needs <= 4 text symbols separable by a 1- or 2-bit field and "
+                             "every pattern symbol present in the text");
   }
   pl.strategy = strategy;
   if (peel == 0) {
@@ -230,7 +270,7 @@ void fill_desc(const Plan& pl, const uint8_t* p, size_t m, uint64_t delta, uint6
     d.k_begin = (delta + a1) / T;
     const uint64_t k_end = (delta + d.A - 1 + a1) / T + 1;
     d.ntiles = k_end - d.k_begin;
-  } else {
+  } else {  // BLOCK and PACKED: tile in alignment space
     d.pre = 0;
     const uint32_t post = (((uint32_t)m - 1) & ~15u) + 16;
     d.stage_len = (uint32_t)T + post;
@@ -265,11 +305,19 @@ void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_
   L.strategy = ps[0]->pl.strategy;
   L.epilogue = epilogue;
   L.e.clear();
+  const bool packed = L.strategy == kPacked1 || L.strategy == kPacked2;
+  const uint32_t cbits = L.strategy == kPacked2 ? 2 : 1;
+  L.a.code_shift = ps[0]->pl.code_shift;
   for (const Planned* q : ps)
-    for (size_t k = 0; k < q->m; ++k) L.e.push_back(q->pl.order[k] | ((uint32_t)q->p[q->pl.order[k]] << 16));
+    for (size_t k = 0; k < q->m; ++k) {
+      const uint32_t sym = q->p[q->pl.order[k]];
+      const uint32_t v = packed ? ((sym >> L.a.code_shift) & ((1u << cbits) - 1u)) : sym;
+      L.e.push_back(q->pl.order[k] | (v << 16));
+    }
   L.a.npat = (uint32_t)ps.size();
   L.a.tbl_words = (uint32_t)L.e.size();
-  L.a.ring_off = (kTblOff + 4 * L.a.tbl_words + 127) & ~127u;
+  L.a.pack_off = (kTblOff + 4 * L.a.tbl_words + 127) & ~127u;
+  L.a.ring_off = L.a.pack_off;
   uint32_t T = ps[0]->pl.tile;
   for (;;) {
     L.a.tile = T;
@@ -288,6 +336,10 @@ void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_
     }
     L.a.total_work = work;
     L.a.stage_stride = (max_stage + 127) & ~127u;
+    if (packed) {  // double-buffered code array: 2b bytes of codes per 16-byte chunk (+ a slack word)
+      L.a.pack_bytes = ((max_stage / 16u) * 2u * cbits + 16u + 127u) & ~127u;
+      L.a.ring_off = L.a.pack_off + 2 * L.a.pack_bytes;
+    }
     // shared memory per SM: 228 KiB, 1 KiB reserved per resident CTA
     int ctas = tunables().ctas_per_sm;
     uint32_t stages = 0;
@@ -365,7 +417,7 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
     plans.push_back(std::move(q));
   }
   // group by strategy (kernel template), keep the caller's order inside a group
-  for (int strat : {(int)kFilter, (int)kBlock}) {
+  for (int strat : {(int)kFilter, (int)kBlock, (int)kPacked1, (int)kPacked2}) {
     std::vector<const Planned*> batch;
     size_t words = 0;
     auto flush = [&]() -> sm_status {
@@ -601,7 +653,7 @@ sm_status sm_count_batch(const uint8_t* const* p, const size_t* m, size_t P, con
                          void* stream) {
   if (P == 0) return SM_OK;
   if (!p || !m || !d_counts) return fail(SM_EINVAL, "NULL argument");
-  if (strategy < SM_STRATEGY_AUTO || strategy > SM_STRATEGY_BLOCK) return fail(SM_EINVAL, "bad strategy");
+  if (strategy < SM_STRATEGY_AUTO || strategy > SM_STRATEGY_PACKED) return fail(SM_EINVAL, "bad strategy");
   for (size_t i = 0; i < P; ++i) {
     if (m[i] == 0) return fail(SM_EINVAL, "m[i] == 0: empty pattern is undefined (reading R2)");
     if (m[i] > SM_MAX_PATTERN) return fail(SM_EINVAL, "m[i] > SM_MAX_PATTERN (4096)");
@@ -622,7 +674,7 @@ sm_status sm_report_batch(const uint8_t* const* p, const size_t* m, size_t P, co
                           uint64_t* d_counts, void* stream) {
   if (P == 0) return SM_OK;
   if (!p || !m || !d_counts) return fail(SM_EINVAL, "NULL argument");
-  if (strategy < SM_STRATEGY_AUTO || strategy > SM_STRATEGY_BLOCK) return fail(SM_EINVAL, "bad strategy");
+  if (strategy < SM_STRATEGY_AUTO || strategy > SM_STRATEGY_PACKED) return fail(SM_EINVAL, "bad strategy");
   for (size_t i = 0; i < P; ++i) {
     if (m[i] == 0) return fail(SM_EINVAL, "m[i] == 0: empty pattern is undefined (reading R2)");
     if (m[i] > SM_MAX_PATTERN) return fail(SM_EINVAL, "m[i] > SM_MAX_PATTERN (4096)");

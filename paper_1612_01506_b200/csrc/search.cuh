@@ -24,7 +24,7 @@ constexpr uint32_t kWarpTotOff = 2 * kMaxStages * 8;
 constexpr uint32_t kQueueOff = kWarpTotOff + 2 * kConsumerWarps * 4;
 constexpr uint32_t kTblOff = kQueueOff + kConsumerWarps * kQueueLen * 2;
 
-enum Strategy : int { kFilter = 1, kBlock = 2 };
+enum Strategy : int { kFilter = 1, kBlock = 2, kPacked1 = 3, kPacked2 = 4 };  // kPackedB: b-bit codes
 enum Epilogue : int { kEpiCount = 0, kEpiTileCount = 1, kEpiWrite = 2 };
 
 // One pattern of a launch.  Byte offsets are relative to `base` = align_down(t, 16);
@@ -62,6 +62,9 @@ struct LaunchArgs {
   uint32_t ring_off;         // smem byte offset of stage 0
   uint32_t npat;             // patterns in the batch
   uint32_t tbl_words;        // table entries
+  uint32_t code_shift;       // PACKED: code(x) = (x >> code_shift) & (2^b - 1), injective on the text's symbols
+  uint32_t pack_off;         // PACKED: smem byte offset of the double-buffered code array
+  uint32_t pack_bytes;       // PACKED: bytes of one code buffer
   uint64_t* tile_counts;     // kEpiTileCount: u64[total_work] per work item (zeroed by host)
   const uint64_t* tile_offsets;  // kEpiWrite: exclusive prefix over work items, total_work + 1 entries
   uint64_t* pos;             // kEpiWrite: output positions
@@ -69,7 +72,8 @@ struct LaunchArgs {
 };
 
 // Kernel parameters: everything per launch, no __constant__ state, so launches on
-// different streams never race.  Table entry = off(pi(k)) | p[pi(k)] << 16.
+// different streams never race.  Table entry = off(pi(k)) | p[pi(k)] << 16
+// (PACKED: the symbol's b-bit code instead of the byte).
 template <int CAP>
 struct LaunchParams {
   LaunchArgs a;

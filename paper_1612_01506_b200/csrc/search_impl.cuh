@@ -276,13 +276,15 @@ __device__ __forceinline__ uint32_t verify_survivors(const Pat& pt, const uint8_
 }
 
 // Positions of one warp's chunk stream, written in ascending order (input: compressed found word).
+// IN_G: input is a compressed found word (FILTER/BLOCK), else a 16-bit mask.
+template <bool IN_G = true>
 struct WriteSink {
   uint64_t run;    // next output index of this warp
   int64_t pbase;   // 0-based position of u = 0
   uint64_t* pos;
   uint64_t cap;
   __device__ __forceinline__ void operator()(uint32_t c, uint32_t g, int lane) {
-    uint32_t m16 = g_to_mask16(g);
+    uint32_t m16 = IN_G ? g_to_mask16(g) : g;
     const uint32_t pc = __popc(m16);
     const uint32_t incl = warp_incl_scan(pc, lane);
     uint64_t idx = run + incl - pc;
@@ -390,6 +392,105 @@ __device__ __forceinline__ void block_tile(const Pat& pt, const uint8_t* buf, ui
   for (int it = 0; it < CPL; ++it) g_out[it] = compress_found(F[it]);  // popcount of found
 }
 
+// ---------------------------------------------------------------------------
+// PACKED strategy (small text alphabets): every text byte is first replaced by a
+// b-bit code, code(x) = (x >> s) & (2^b - 1), injective on the symbols of t (the
+// host checks it on the histogram), and the packed codes of a tile are kept in
+// shared memory.  A comparison step (Alg. 4) for pattern
+// position pi(k) over 16 alignments is then a funnel shift of two code words, an
+// XNOR with the broadcast code and an AND -- the SIMDcompare of PAPER.md:94 on
+// b-bit lanes instead of 8-bit ones.  Same result as comparing bytes.
+// ---------------------------------------------------------------------------
+template <int B>
+__device__ __forceinline__ uint32_t pack4(uint32_t w, uint32_t s) {
+  if (B == 2) return (((w >> s) & 0x03030303u) * 0x01041040u) >> 24;  // byte k's code -> bits 2k, 2k+1
+  return (((w >> s) & 0x01010101u) * 0x01020408u) >> 24;                 // byte k's code -> bit k
+}
+template <int B>
+__device__ __forceinline__ uint32_t pack_chunk(const uint4 v, uint32_t s) {
+  return pack4<B>(v.x, s) | (pack4<B>(v.y, s) << (4 * B)) | (pack4<B>(v.z, s) << (8 * B)) |
+         (pack4<B>(v.w, s) << (12 * B));
+}
+template <int B>
+__device__ __forceinline__ void store_codes(uint8_t* pk, uint32_t c, uint32_t codes) {
+  if (B == 2) reinterpret_cast<uint32_t*>(pk)[c] = codes;
+  else reinterpret_cast<uint16_t*>(pk)[c] = (uint16_t)codes;
+}
+// bit j -> bit 2j (16 -> 32 bits)
+__device__ __forceinline__ uint32_t spread2(uint32_t x) {
+  x = (x | (x << 8)) & 0x00FF00FFu;
+  x = (x | (x << 4)) & 0x0F0F0F0Fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  return (x | (x << 1)) & 0x55555555u;
+}
+// bit 2j -> bit j
+__device__ __forceinline__ uint32_t gather2(uint32_t x) {
+  x &= 0x55555555u;
+  x = (x | (x >> 1)) & 0x33333333u;
+  x = (x | (x >> 2)) & 0x0F0F0F0Fu;
+  x = (x | (x >> 4)) & 0x00FF00FFu;
+  return (x | (x >> 8)) & 0x0000FFFFu;
+}
+
+// found &= [code of position 16c + off + j == code] for j = 0..15 (flag of alignment j
+// at bit j (b = 1) or bit 2j (b = 2)).
+template <int B>
+__device__ __forceinline__ uint32_t packed_eq(const uint32_t* pk32, uint32_t c, uint32_t off, uint32_t ccode) {
+  const uint32_t v = 16u * c + off;                      // first position compared
+  const uint32_t q = B == 2 ? (v >> 4) : (v >> 5);       // code word holding it
+  const uint32_t sh = B == 2 ? (v & 15u) * 2u : (v & 31u);
+  const uint32_t w = __funnelshift_r(pk32[q], pk32[q + 1], sh);
+  if (B == 2) {
+    const uint32_t e = ~(w ^ (ccode * 0x55555555u));
+    return e & (e >> 1);  // even bit 2j set iff both code bits equal
+  }
+  return ~(w ^ (0u - ccode));
+}
+
+// One warp's share of a PACKED tile: pack this lane's chunks (and a share of the
+// halo), then -- after the CTA's consumer warps have packed the whole tile --
+// Alg. 4 on the codes: r peeled steps, then the pi-ordered loop with a warp-uniform
+// exit test.  Returns per-chunk 16-bit match masks.
+template <int CPL, int B>
+__device__ __forceinline__ void packed_tile(const Pat& pt, const uint8_t* buf, uint8_t* pk, uint32_t nchunks,
+                                            uint32_t code_shift, uint32_t cw0, int warp, int lane, bool edge,
+                                            int32_t rlo, int32_t rhi, uint64_t* empty_bar, uint32_t* m_out) {
+#pragma unroll
+  for (int it = 0; it < CPL; ++it) {
+    const uint32_t c = cw0 + it * 32u + lane;
+    store_codes<B>(pk, c, pack_chunk<B>(lds128(buf + 16u * c), code_shift));
+  }
+  for (uint32_t c = (uint32_t)CPL * kLanesPerTilePass + warp * 32u + lane; c < nchunks; c += kLanesPerTilePass)
+    store_codes<B>(pk, c, pack_chunk<B>(lds128(buf + 16u * c), code_shift));  // halo chunks
+  __syncwarp();
+  if (lane == 0) mbar_arrive(empty_bar);  // the stage's bytes are no longer needed
+  named_bar_sync(1, kConsumerWarps * 32);  // all codes of the tile are in place
+  const uint32_t* pk32 = reinterpret_cast<const uint32_t*>(pk);
+  uint32_t F[CPL];
+#pragma unroll
+  for (int it = 0; it < CPL; ++it) {
+    const uint32_t vm = edge ? range_mask16_rel((int32_t)(16u * (cw0 + it * 32u + lane)), rlo, rhi) : 0xFFFFu;
+    F[it] = B == 2 ? spread2(vm) : vm;
+  }
+  uint32_t k = 0;
+  for (; k < pt.r; ++k) {  // peeled: all r comparisons, no test
+    const uint32_t e = pt.tbl[k];
+#pragma unroll
+    for (int it = 0; it < CPL; ++it) F[it] &= packed_eq<B>(pk32, cw0 + it * 32u + lane, e & 0xFFFFu, e >> 16);
+  }
+  for (; k < pt.m; ++k) {  // ordered loop with exit test, warp-uniform
+    uint32_t any = 0;
+#pragma unroll
+    for (int it = 0; it < CPL; ++it) any |= F[it];
+    if (!__any_sync(0xFFFFFFFFu, any != 0)) break;
+    const uint32_t e = pt.tbl[k];
+#pragma unroll
+    for (int it = 0; it < CPL; ++it) F[it] &= packed_eq<B>(pk32, cw0 + it * 32u + lane, e & 0xFFFFu, e >> 16);
+  }
+#pragma unroll
+  for (int it = 0; it < CPL; ++it) m_out[it] = B == 2 ? gather2(F[it]) : (F[it] & 0xFFFFu);
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -426,7 +527,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
   uint16_t* qc = reinterpret_cast<uint16_t*>(smem + kQueueOff) + warp * kQueueLen;
   const uint32_t T = a.tile;
   const uint32_t cw0 = (uint32_t)warp * 32u * CPL;  // first chunk of this warp
-  uint32_t s = 0, ph = 0, par = 0;
+  uint32_t s = 0, ph = 0, par = 0, par_pk = 0;
   uint32_t k = 0;
   uint32_t acc = 0;  // kEpiCount: this lane's matches of pattern k so far
   for (uint64_t w = blockIdx.x; w < a.total_work; w += gridDim.x) {
@@ -473,9 +574,36 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
         const uint32_t wtot = __reduce_add_sync(0xFFFFFFFFu, cs.n);
         if (lane == 0) s_wt[par * kConsumerWarps + warp] = wtot;
         named_bar_sync(1, kConsumerWarps * 32);
-        WriteSink ws{a.tile_offsets[w], x_base - (int64_t)a.delta, a.pos, a.cap};
+        WriteSink<> ws{a.tile_offsets[w], x_base - (int64_t)a.delta, a.pos, a.cap};
         for (int wv = 0; wv < warp; ++wv) ws.run += s_wt[par * kConsumerWarps + wv];
         filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, ws);
+        par ^= 1u;
+      }
+    } else if (STRAT == kPacked1 || STRAT == kPacked2) {
+      constexpr int B = STRAT == kPacked2 ? 2 : 1;
+      uint32_t mk[CPL];
+      uint8_t* pk = smem + a.pack_off + par_pk * a.pack_bytes;
+      packed_tile<CPL, B>(pt, buf, pk, d.stage_len / 16u, a.code_shift, cw0, warp, lane, edge, rlo, rhi, &empty[s], mk);
+      par_pk ^= 1u;
+      uint32_t tc = 0;
+#pragma unroll
+      for (int it = 0; it < CPL; ++it) tc += __popc(mk[it]);
+      if (EPI == kEpiCount) {
+        acc += tc;
+      } else if (EPI == kEpiTileCount) {
+        const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, tc);
+        if (lane == 0 && ws) {
+          atomicAdd(reinterpret_cast<unsigned long long*>(&a.tile_counts[w]), (unsigned long long)ws);
+          atomicAdd(reinterpret_cast<unsigned long long*>(d.count_out), (unsigned long long)ws);
+        }
+      } else {
+        const uint32_t wtot = __reduce_add_sync(0xFFFFFFFFu, tc);
+        if (lane == 0) s_wt[par * kConsumerWarps + warp] = wtot;
+        named_bar_sync(1, kConsumerWarps * 32);
+        WriteSink<false> ws{a.tile_offsets[w], x_base - (int64_t)a.delta, a.pos, a.cap};
+        for (int wv = 0; wv < warp; ++wv) ws.run += s_wt[par * kConsumerWarps + wv];
+#pragma unroll
+        for (int it = 0; it < CPL; ++it) ws(cw0 + it * 32u + lane, mk[it], lane);
         par ^= 1u;
       }
     } else {
@@ -496,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
         const uint32_t wtot = __reduce_add_sync(0xFFFFFFFFu, tc);
         if (lane == 0) s_wt[par * kConsumerWarps + warp] = wtot;
         named_bar_sync(1, kConsumerWarps * 32);
-        WriteSink ws{a.tile_offsets[w], x_base - (int64_t)a.delta, a.pos, a.cap};
+        WriteSink<> ws{a.tile_offsets[w], x_base - (int64_t)a.delta, a.pos, a.cap};
         for (int wv = 0; wv < warp; ++wv) ws.run += s_wt[par * kConsumerWarps + wv];
 #pragma unroll
         for (int it = 0; it < CPL; ++it) ws(cw0 + it * 32u + lane, g[it], lane);
@@ -505,7 +633,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
     }
 
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    if (STRAT != kPacked1 && STRAT != kPacked2 && lane == 0) mbar_arrive(&empty[s]);  // PACKED released it after packing
     if (++s == a.stages) {
       s = 0;
       ph ^= 1u;

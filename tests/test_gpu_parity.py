@@ -334,3 +334,61 @@ def test_report_batch_concatenated(sm):
             sm.sm_report_batch(pats, t, pos[:cap] if cap else None, d, hist=oracle.hist(a))
             assert d.cpu().tolist() == want_cnt
             assert pos[:cap].cpu().numpy().astype(np.uint64).tolist() == flat[:cap].tolist(), (sigma, cap)
+
+
+# ------------------------------------------------------------------------------------------- PACKED (b-bit codes)
+PACKED_ALPHABETS = [b"ACGT", b"\x00\x01", b"a", b"ab", b"\x10\x30", b"ACG", b"\x00\x40\x80\xc0"]
+
+
+def test_packed_strategy_matches_oracle(sm):
+    rng = np.random.default_rng(31337)
+    for alpha in PACKED_ALPHABETS:
+        syms = np.frombuffer(alpha, dtype=np.uint8)
+        for n in (1, 15, 16, 17, 5000, 70001, 1 << 20):
+            a = syms[rng.integers(0, syms.size, n)]
+            h = oracle.hist(a)
+            for m in (1, 2, 5, 16, 31, 64, 300):
+                if m > n:
+                    continue
+                s = int(rng.integers(0, n - m + 1))
+                p = a[s:s + m].tobytes()
+                off = int(rng.integers(0, 16))
+                t = dev(a, off)
+                want = oracle.naive_count(p, a)
+                peel = int(rng.integers(0, m + 1))
+                assert count_async(sm, p, t, hist=h, strategy=sm.SM_STRATEGY_PACKED, peel=peel) == want, \
+                    (alpha, n, m, off, peel)
+                if n <= 70001:
+                    pos, total = report_async(sm, p, t, cap=want + 1, hist=h, strategy=sm.SM_STRATEGY_PACKED)
+                    assert total == want and pos.astype(np.uint64).tolist() == oracle.naive_report(p, a).tolist()
+
+
+def test_packed_applicability(sm):
+    a = np.frombuffer(b"ACGT" * 1000, dtype=np.uint8)
+    h = oracle.hist(a)
+    s, r = sm.sm_plan(b"ACGTACGTAC", h)
+    assert s == 4                                  # AUTO picks 2-bit codes for DNA
+    with pytest.raises(sm.SmError):                # 'N' is absent from the text: not packable
+        sm.sm_plan(b"ACGN", h, strategy=sm.SM_STRATEGY_PACKED)
+    b = np.frombuffer(bytes(range(5)) * 100, dtype=np.uint8)
+    with pytest.raises(sm.SmError):                # 5 symbols > 4
+        sm.sm_plan(b"\x00\x01", oracle.hist(b), strategy=sm.SM_STRATEGY_PACKED)
+    c = np.frombuffer(b"\x00\x01" * 100, dtype=np.uint8)
+    assert sm.sm_plan(b"\x01\x00\x01", oracle.hist(c))[0] == 3   # binary: 1-bit codes
+
+
+def test_packed_batch_and_dense_report(sm):
+    rng = np.random.default_rng(4)
+    a = np.frombuffer(b"ACGT", dtype=np.uint8)[rng.integers(0, 4, 3_000_017)]
+    t = dev(a, 5)
+    pats = [a[s:s + m].tobytes() for m in (1, 2, 4, 8, 12, 32, 100) for s in rng.integers(0, a.size - m, 5)]
+    d = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
+    sm.sm_count_batch(pats, t, d, strategy=sm.SM_STRATEGY_PACKED)
+    want = [oracle.naive_count(p, a) for p in pats]
+    assert d.cpu().tolist() == want
+    sub = pats[:10]
+    cap = sum(want[:10])
+    pos = torch.zeros(cap, dtype=torch.int64, device="cuda")
+    d2 = torch.zeros(10, dtype=torch.int64, device="cuda")
+    sm.sm_report_batch(sub, t, pos, d2)  # AUTO -> PACKED
+    assert np.array_equal(pos.cpu().numpy().astype(np.uint64), np.concatenate([oracle.naive_report(p, a) for p in sub]))

@@ -38,6 +38,14 @@ for ps in pats:
     f = [float(hist[ps.data[j]]) / tot for j in order]
     row = {"cfg": a.config, "m": ps.m, "f": [round(x, 5) for x in f[:6]], "auto": sm.sm_plan(ps.data, hist)}
     row["filter"] = round(timeit(ps.data, 1, 0), 2)
+    try:
+        sm.sm_plan(ps.data, hist, strategy=3)
+        for r in (1, 2, 4, 6, 8, 12):
+            if r <= ps.m:
+                row[f"packed{r}"] = round(timeit(ps.data, 3, r), 2)
+        row["packed_auto"] = round(timeit(ps.data, 3, 0), 2)
+    except sm.SmError:
+        pass
     for r in (1, 2, 3, 4, 6):
         if r <= ps.m:
             row[f"block{r}"] = round(timeit(ps.data, 2, r), 2)
