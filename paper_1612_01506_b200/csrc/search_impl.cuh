@@ -432,19 +432,44 @@ __device__ __forceinline__ uint32_t gather2(uint32_t x) {
   return (x | (x >> 8)) & 0x0000FFFFu;
 }
 
-// found &= [code of position 16c + off + j == code] for j = 0..15 (flag of alignment j
-// at bit j (b = 1) or bit 2j (b = 2)).
-template <int B>
-__device__ __forceinline__ uint32_t packed_eq(const uint32_t* pk32, uint32_t c, uint32_t off, uint32_t ccode) {
-  const uint32_t v = 16u * c + off;                      // first position compared
-  const uint32_t q = B == 2 ? (v >> 4) : (v >> 5);       // code word holding it
-  const uint32_t sh = B == 2 ? (v & 15u) * 2u : (v & 31u);
-  const uint32_t w = __funnelshift_r(pk32[q], pk32[q + 1], sh);
-  if (B == 2) {
-    const uint32_t e = ~(w ^ (ccode * 0x55555555u));
-    return e & (e >> 1);  // even bit 2j set iff both code bits equal
+// One PACKED comparison step over the CPL chunks of a lane: F[it] &= [code of
+// position 16c + off + j == ccode] for j = 0..15 (flag of alignment j at bit j for
+// b = 1, bit 2j for b = 2).  W0/W1 = the code words holding positions 16c.. (kept in
+// registers, so steps with off < 16 need no shared-memory load).  All branches
+// are warp-uniform and taken once per step.
+template <int CPL, int B>
+__device__ __forceinline__ void packed_step(uint32_t (&F)[CPL], const uint32_t (&W0)[CPL], const uint32_t (&W1)[CPL],
+                                            const uint32_t* pk32, uint32_t qbase, int lane, uint32_t e) {
+  const uint32_t off = e & 0xFFFFu, ccode = e >> 16;
+  const uint32_t rep = B == 2 ? ccode * 0x55555555u : 0u - ccode;
+  // bit offset of position 16c + off relative to the start of W0 (lane parity matters for b = 1)
+  const uint32_t u = B == 2 ? 2u * off : 16u * (uint32_t)(lane & 1) + off;
+  if (off < 16u) {  // warp-uniform; then u < 32 on every lane
+#pragma unroll
+    for (int it = 0; it < CPL; ++it) {
+      const uint32_t w = __funnelshift_r(W0[it], W1[it], u);
+      if (B == 2) {
+        const uint32_t x = ~(w ^ rep);
+        F[it] &= x & (x >> 1);
+      } else {
+        F[it] &= ~(w ^ rep);
+      }
+    }
+  } else {
+    const uint32_t* p = pk32 + qbase + (u >> 5);  // word of chunk it at p[it * (B == 2 ? 32 : 16)]
+    const uint32_t sh = u & 31u;
+#pragma unroll
+    for (int it = 0; it < CPL; ++it) {
+      const uint32_t* pw = p + it * (B == 2 ? 32 : 16);
+      const uint32_t w = __funnelshift_r(pw[0], pw[1], sh);
+      if (B == 2) {
+        const uint32_t x = ~(w ^ rep);
+        F[it] &= x & (x >> 1);
+      } else {
+        F[it] &= ~(w ^ rep);
+      }
+    }
   }
-  return ~(w ^ (0u - ccode));
 }
 
 // One warp's share of a PACKED tile: pack this lane's chunks (and a share of the
@@ -466,26 +491,24 @@ __device__ __forceinline__ void packed_tile(const Pat& pt, const uint8_t* buf, u
   if (lane == 0) mbar_arrive(empty_bar);  // the stage's bytes are no longer needed
   named_bar_sync(1, kConsumerWarps * 32);  // all codes of the tile are in place
   const uint32_t* pk32 = reinterpret_cast<const uint32_t*>(pk);
-  uint32_t F[CPL];
+  const uint32_t qbase = B == 2 ? (cw0 + lane) : ((cw0 + lane) >> 1);  // code word of chunk it = 0
+  uint32_t F[CPL], W0[CPL], W1[CPL];
 #pragma unroll
   for (int it = 0; it < CPL; ++it) {
     const uint32_t vm = edge ? range_mask16_rel((int32_t)(16u * (cw0 + it * 32u + lane)), rlo, rhi) : 0xFFFFu;
     F[it] = B == 2 ? spread2(vm) : vm;
+    const uint32_t q = qbase + it * (B == 2 ? 32 : 16);
+    W0[it] = pk32[q];
+    W1[it] = pk32[q + 1];
   }
   uint32_t k = 0;
-  for (; k < pt.r; ++k) {  // peeled: all r comparisons, no test
-    const uint32_t e = pt.tbl[k];
-#pragma unroll
-    for (int it = 0; it < CPL; ++it) F[it] &= packed_eq<B>(pk32, cw0 + it * 32u + lane, e & 0xFFFFu, e >> 16);
-  }
+  for (; k < pt.r; ++k) packed_step<CPL, B>(F, W0, W1, pk32, qbase, lane, pt.tbl[k]);  // peeled
   for (; k < pt.m; ++k) {  // ordered loop with exit test, warp-uniform
     uint32_t any = 0;
 #pragma unroll
     for (int it = 0; it < CPL; ++it) any |= F[it];
     if (!__any_sync(0xFFFFFFFFu, any != 0)) break;
-    const uint32_t e = pt.tbl[k];
-#pragma unroll
-    for (int it = 0; it < CPL; ++it) F[it] &= packed_eq<B>(pk32, cw0 + it * 32u + lane, e & 0xFFFFu, e >> 16);
+    packed_step<CPL, B>(F, W0, W1, pk32, qbase, lane, pt.tbl[k]);
   }
 #pragma unroll
   for (int it = 0; it < CPL; ++it) m_out[it] = B == 2 ? gather2(F[it]) : (F[it] & 0xFFFFu);
