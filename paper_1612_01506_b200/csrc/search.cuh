@@ -17,7 +17,7 @@ constexpr uint32_t kLaneVerifyMaxM = 34;                 // FILTER: per-lane ver
 constexpr int kMaxBatch = 32;                            // patterns per launch
 constexpr int kTableSmall = 256;                         // pattern-table capacities (u32 entries)
 constexpr int kTableLarge = 4096;
-constexpr int kBatchTableWords = 1024;                 // batching: table entries per launch (3 x 32 KiB stages fit)
+constexpr int kBatchTableWords = 2048;                 // batching: table entries per launch (3 x 32 KiB stages fit for m <= 1024)
 
 // shared-memory layout: [full/empty mbarriers][warp totals [2][W]][queue chunk ids u16 [W][kQueueLen]][table][ring]
 constexpr uint32_t kWarpTotOff = 2 * kMaxStages * 8;
