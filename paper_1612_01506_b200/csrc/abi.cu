@@ -316,7 +316,7 @@ void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_
     }
   L.a.npat = (uint32_t)ps.size();
   L.a.tbl_words = (uint32_t)L.e.size();
-  L.a.pack_off = (kTblOff + 4 * L.a.tbl_words + 127) & ~127u;
+  L.a.pack_off = (kTblOff + 127) & ~127u;
   L.a.ring_off = L.a.pack_off;
   uint32_t T = ps[0]->pl.tile;
   for (;;) {
@@ -407,37 +407,36 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
     if (s != SM_OK) return s;
     h = hb;
   }
-  std::vector<Planned> plans;
-  plans.reserve(P);
+  // plan and launch as we go: a batch is launched as soon as it is full, so the GPU
+  // starts on the first patterns while the host still orders the later ones
+  std::vector<Planned> plans(P);
+  constexpr int kStrategies = 5;                  // index = strategy value (1..4)
+  std::vector<const Planned*> batch[kStrategies];
+  size_t words[kStrategies] = {0, 0, 0, 0, 0};
+  auto flush = [&](int strat) -> sm_status {
+    if (batch[strat].empty()) return SM_OK;
+    HostLaunch L;
+    build_launch(batch[strat], t, n, lim, kEpiCount, L);
+    batch[strat].clear();
+    words[strat] = 0;
+    return launch_checked(L, st, "search kernel (batch)");
+  };
   for (size_t i = 0; i < P; ++i) {
     if (n < ms[i] || lim == 0) continue;  // count stays 0
-    Planned q{Plan(), ps[i], ms[i], d_counts + i};
+    Planned& q = plans[i];
+    q = Planned{Plan(), ps[i], ms[i], d_counts + i};
     sm_status s = make_plan(ps[i], ms[i], n, h, nullptr, 0, strategy, q.pl);
     if (s != SM_OK) return s;
-    plans.push_back(std::move(q));
-  }
-  // group by strategy (kernel template), keep the caller's order inside a group
-  for (int strat : {(int)kFilter, (int)kBlock, (int)kPacked1, (int)kPacked2}) {
-    std::vector<const Planned*> batch;
-    size_t words = 0;
-    auto flush = [&]() -> sm_status {
-      if (batch.empty()) return SM_OK;
-      HostLaunch L;
-      build_launch(batch, t, n, lim, kEpiCount, L);
-      batch.clear();
-      words = 0;
-      return launch_checked(L, st, "search kernel (batch)");
-    };
-    for (const Planned& q : plans) {
-      if (q.pl.strategy != strat) continue;
-      if (batch.size() == (size_t)kMaxBatch || words + q.m > (size_t)kBatchTableWords) {
-        sm_status s = flush();
-        if (s != SM_OK) return s;
-      }
-      batch.push_back(&q);
-      words += q.m;
+    const int k = q.pl.strategy;
+    if (batch[k].size() == (size_t)kMaxBatch || words[k] + q.m > (size_t)kBatchTableWords) {
+      s = flush(k);
+      if (s != SM_OK) return s;
     }
-    sm_status s = flush();
+    batch[k].push_back(&q);
+    words[k] += q.m;
+  }
+  for (int k = 1; k < kStrategies; ++k) {
+    sm_status s = flush(k);
     if (s != SM_OK) return s;
   }
   return SM_OK;

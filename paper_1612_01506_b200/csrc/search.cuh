@@ -16,13 +16,14 @@ constexpr int kQueueLen = 32 * kGroup;                   // FILTER: queue entrie
 constexpr uint32_t kLaneVerifyMaxM = 34;                 // FILTER: per-lane verification up to this m
 constexpr int kMaxBatch = 32;                            // patterns per launch
 constexpr int kTableSmall = 256;                         // pattern-table capacities (u32 entries)
-constexpr int kTableLarge = 4096;
-constexpr int kBatchTableWords = 2048;                 // batching: table entries per launch (3 x 32 KiB stages fit for m <= 1024)
+constexpr int kTableLarge = 7168;                        // fills the 32 KiB kernel-parameter space
+constexpr int kBatchTableWords = kTableLarge;            // batching: table entries per launch
 
-// shared-memory layout: [full/empty mbarriers][warp totals [2][W]][queue chunk ids u16 [W][kQueueLen]][table][ring]
+// shared-memory layout: [full/empty mbarriers][warp totals [2][W]][queue chunk ids u16 [W][kQueueLen]]
+//                       [PACKED code buffers][ring]   (the pattern tables stay in the kernel parameters)
 constexpr uint32_t kWarpTotOff = 2 * kMaxStages * 8;
 constexpr uint32_t kQueueOff = kWarpTotOff + 2 * kConsumerWarps * 4;
-constexpr uint32_t kTblOff = kQueueOff + kConsumerWarps * kQueueLen * 2;
+constexpr uint32_t kTblOff = kQueueOff + kConsumerWarps * kQueueLen * 2;  // end of the fixed region
 
 enum Strategy : int { kFilter = 1, kBlock = 2, kPacked1 = 3, kPacked2 = 4 };  // kPackedB: b-bit codes
 enum Epilogue : int { kEpiCount = 0, kEpiTileCount = 1, kEpiWrite = 2 };
@@ -47,7 +48,7 @@ struct PatDesc {
   uint32_t bc2;        // p[pi(2)] * 0x01010101 (FILTER, m >= 2)
   uint32_t pre;        // buffer bytes before the tile (multiple of 16)
   uint32_t stage_len;  // bytes the tile's buffer holds = T + pre + post (multiple of 16)
-  uint32_t tbl;        // index of this pattern's first entry in the shared table
+  uint32_t tbl;        // index of this pattern's first entry in LaunchParams::e
   uint32_t pad_;
 };
 
@@ -80,5 +81,6 @@ struct LaunchParams {
   PatDesc d[kMaxBatch];
   uint32_t e[CAP];
 };
+static_assert(sizeof(LaunchParams<kTableLarge>) <= 32764, "kernel parameter space is 32764 bytes on sm_100a");
 
 }  // namespace smgpu

@@ -131,7 +131,7 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 // Per-tile view of one pattern of the batch (read from the kernel parameters).
 struct Pat {
   uint32_t m, r, a1, bc1, s2, bc2, pre;
-  const uint32_t* tbl;  // shared-memory table of this pattern (m entries, pi order)
+  const uint32_t* tbl;  // this pattern's table in the kernel parameters (m entries, pi order; constant cache)
 };
 
 // ---------------------------------------------------------------------------
@@ -361,6 +361,11 @@ __device__ __forceinline__ void block_step_q(Found4 (&F)[CPL], const uint8_t* cb
 template <int CPL>
 __device__ __forceinline__ void block_step(Found4 (&F)[CPL], const uint8_t* cbase, uint32_t e) {
   const uint32_t off = e & 0xFFFFu, bc = (e >> 16) * 0x01010101u;
+  if ((off & 15u) == 0) {  // 16-B aligned window: one LDS.128, no shifts
+#pragma unroll
+    for (int it = 0; it < CPL; ++it) found_and_eq(F[it], lds128(cbase + off + it * 512u), bc);
+    return;
+  }
   switch ((off >> 2) & 3u) {  // warp-uniform
     case 0: block_step_q<CPL, 0>(F, cbase, off, bc); break;
     case 1: block_step_q<CPL, 1>(F, cbase, off, bc); break;
@@ -528,11 +533,9 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + kMaxStages;
   uint32_t* s_wt = reinterpret_cast<uint32_t*>(smem + kWarpTotOff);  // [2][W]
-  uint32_t* tbl = reinterpret_cast<uint32_t*>(smem + kTblOff);
   uint8_t* ring = smem + a.ring_off;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (uint32_t q = threadIdx.x; q < a.tbl_words; q += blockDim.x) tbl[q] = P.e[q];
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < a.stages; ++s) {
       mbar_init(&full[s], 1);
@@ -567,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
     if (EPI == kEpiWrite && a.tile_offsets[w + 1] == a.tile_offsets[w]) continue;
     mbar_wait(&full[s], ph);
     const uint8_t* buf = ring + (size_t)s * a.stage_stride;
-    const Pat pt{d.m, d.r, d.a1, d.bc1, d.s2, d.bc2, d.pre, tbl + d.tbl};
+    const Pat pt{d.m, d.r, d.a1, d.bc1, d.s2, d.bc2, d.pre, P.e + d.tbl};
     const bool edge = ti < d.edge_lo || ti >= d.edge_hi;  // tile holds invalid alignments
     const int64_t shift = (STRAT == kFilter) ? (int64_t)d.a1 : 0;
     const int64_t x_base = (int64_t)((d.k_begin + ti) * T) - shift;  // alignment offset of u = 0
