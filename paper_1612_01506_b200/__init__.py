@@ -28,7 +28,8 @@ from typing import Optional, Sequence, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsmgpu.so")
+# SMGPU_LIB=debug selects the bounds-checked build (libsmgpu_debug.so, tests only)
+LIB_PATH = os.path.join(_HERE, "libsmgpu_debug.so" if os.environ.get("SMGPU_LIB") == "debug" else "libsmgpu.so")
 
 SM_OK, SM_EINVAL, SM_ETRUNC, SM_ENOMEM, SM_ECUDA = 0, 1, 2, 3, 4
 SM_STRATEGY_AUTO, SM_STRATEGY_FILTER, SM_STRATEGY_BLOCK, SM_STRATEGY_PACKED = 0, 1, 2, 3

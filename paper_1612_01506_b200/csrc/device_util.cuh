@@ -5,6 +5,25 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Debug build (-DSMGPU_DEBUG_CHECKS, libsmgpu_debug.so): device-side bounds
+// assertions on every global read range and shared-memory window (a stand-in for
+// compute-sanitizer, which is not available on this pool).  Compiled out otherwise.
+#ifdef SMGPU_DEBUG_CHECKS
+#include <cstdio>
+#define SMGPU_DCHECK(cond)                                                              \
+  do {                                                                                  \
+    if (!(cond)) {                                                                      \
+      printf("SMGPU_DCHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x, #cond);                                 \
+      __trap();                                                                         \
+    }                                                                                   \
+  } while (0)
+#else
+#define SMGPU_DCHECK(cond) \
+  do {                     \
+  } while (0)
+#endif
+
 namespace smgpu {
 
 // ---------------------------------------------------------------------------

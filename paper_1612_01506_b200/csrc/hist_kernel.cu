@@ -28,6 +28,7 @@ __global__ void __launch_bounds__(kHistWarps * 32) hist_kernel(const uint8_t* __
 
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  SMGPU_DCHECK(head <= n && head + nvec * 16 <= n);
   // 2 loads in flight per thread per iteration
   for (; i + stride < nvec; i += 2 * stride) {
     const uint4 a = ldg_v4_stream(v + i, pol);

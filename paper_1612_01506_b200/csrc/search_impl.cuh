@@ -131,6 +131,7 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 // Per-tile view of one pattern of the batch (read from the kernel parameters).
 struct Pat {
   uint32_t m, r, a1, bc1, s2, bc2, pre;
+  uint32_t lim;         // bytes of the tile's stage buffer that hold this pattern's data (stage_len)
   const uint32_t* tbl;  // this pattern's table in the kernel parameters (m entries, pi order; constant cache)
 };
 
@@ -159,9 +160,11 @@ __device__ void produce(const LaunchParams<CAP>& P, uint8_t* ring, uint64_t* ful
     const int64_t vlo = imax(lo, tlo), vhi = imin(hi, thi);
     uint32_t tx = 0;
     int64_t alo = 0;
+    SMGPU_DCHECK(hi - lo <= (int64_t)a.stage_stride);
     if (vlo < vhi) {
       alo = (vlo + 15) & ~(int64_t)15;
       const int64_t ahi = vhi & ~(int64_t)15;
+      SMGPU_DCHECK(vlo >= tlo && vhi <= thi);  // never a byte outside t[0..n)
       bool ragged = false;
       if (alo < ahi) {
         for (int64_t o = vlo; o < alo; ++o) { buf[o - lo] = ldg_u8_nc(a.base + o); ragged = true; }
@@ -173,6 +176,7 @@ __device__ void produce(const LaunchParams<CAP>& P, uint8_t* ring, uint64_t* ful
       if (ragged) fence_proxy_async_smem();
     }
     mbar_arrive_expect_tx(&full[s], tx);
+    SMGPU_DCHECK(tx == 0 || (alo >= tlo && alo + tx <= thi && alo - lo + tx <= (int64_t)d.stage_len));
     if (tx) tma_load_1d(buf + (alo - lo), a.base + alo, tx, &full[s], pol);
     if (++s == a.stages) {
       s = 0;
@@ -216,6 +220,7 @@ __device__ __forceinline__ uint32_t filter_entry(const Pat& pt, const uint8_t* b
                                                  int32_t rlo, int32_t rhi) {
   Found4 F = edge ? found_from_mask16(range_mask16_rel((int32_t)(16u * c), rlo, rhi)) : found_all();
   found_and_eq(F, lds128(buf + pt.pre + 16u * c), pt.bc1);  // pi(1)
+  SMGPU_DCHECK(pt.m < 2 || 16u * c + (pt.s2 & ~15u) + 32u <= pt.lim);
   if (pt.m >= 2)                                               // pi(2)
     found_and_eq(F, window16_q<Q>(buf + 16u * c + (pt.s2 & ~15u), (pt.s2 & 3u) * 8u), pt.bc2);
   return compress_found(F);
@@ -237,6 +242,7 @@ __device__ __forceinline__ uint32_t verify_survivors(const Pat& pt, const uint8_
       const uint8_t* xp = xb + gbit_to_alignment(p);
       for (uint32_t q = 2; q < pt.m; ++q) {
         const uint32_t e = pt.tbl[q];
+        SMGPU_DCHECK((uint32_t)(xp - buf) + (e & 0xFFFFu) < pt.lim);
         if (xp[e & 0xFFFFu] != (e >> 16)) {
           g &= ~(1u << p);
           break;
@@ -262,6 +268,7 @@ __device__ __forceinline__ uint32_t verify_survivors(const Pat& pt, const uint8_
         bool mis = false;
         if (q < pt.m) {
           const uint32_t e = pt.tbl[q];
+          SMGPU_DCHECK((uint32_t)(xp - buf) + (e & 0xFFFFu) < pt.lim);
           mis = xp[e & 0xFFFFu] != (e >> 16);
         }
         if (__any_sync(0xFFFFFFFFu, mis)) {
@@ -333,6 +340,7 @@ __device__ __forceinline__ void filter_tile(const Pat& pt, const uint8_t* buf, u
 #pragma unroll
     for (int it = g0; it < g0 + G; ++it) {
       const uint32_t c = cw0 + it * 32u + lane;
+      SMGPU_DCHECK(pt.pre + 16u * c + 16u <= pt.lim);
       const bool hit = chunk_hit(lds128(buf + pt.pre + 16u * c), pt.bc1);
       const uint32_t bal = __ballot_sync(0xFFFFFFFFu, hit);
       if (hit) qc[qlen + __popc(bal & lanemask_lt())] = (uint16_t)c;
@@ -385,14 +393,22 @@ __device__ __forceinline__ void block_tile(const Pat& pt, const uint8_t* buf, ui
                  : found_all();
   const uint8_t* cbase = buf + 16u * (cw0 + lane);  // chunk it of this lane is at cbase + 512 * it
   uint32_t k = 0;
-  for (; k < pt.r; ++k) block_step<CPL>(F, cbase, pt.tbl[k]);  // peeled: all r, no test
+  // every window of a step lies inside the stage: 16c + (off & ~15) + 32 <= stage_len
+#define SMGPU_BLOCK_DCHECK(e) \
+  SMGPU_DCHECK(16u * (cw0 + (CPL - 1) * 32u + lane) + (((e) & 0xFFFFu) & ~15u) + 32u <= pt.lim)
+  for (; k < pt.r; ++k) {  // peeled: all r, no test
+    SMGPU_BLOCK_DCHECK(pt.tbl[k]);
+    block_step<CPL>(F, cbase, pt.tbl[k]);
+  }
   for (; k < pt.m; ++k) {  // ordered loop with exit test, warp-uniform
     uint32_t any = 0;
 #pragma unroll
     for (int it = 0; it < CPL; ++it) any |= found_any(F[it]);
     if (!__any_sync(0xFFFFFFFFu, any != 0)) break;
+    SMGPU_BLOCK_DCHECK(pt.tbl[k]);
     block_step<CPL>(F, cbase, pt.tbl[k]);
   }
+#undef SMGPU_BLOCK_DCHECK
 #pragma unroll
   for (int it = 0; it < CPL; ++it) g_out[it] = compress_found(F[it]);  // popcount of found
 }
@@ -444,7 +460,8 @@ __device__ __forceinline__ uint32_t gather2(uint32_t x) {
 // are warp-uniform and taken once per step.
 template <int CPL, int B>
 __device__ __forceinline__ void packed_step(uint32_t (&F)[CPL], const uint32_t (&W0)[CPL], const uint32_t (&W1)[CPL],
-                                            const uint32_t* pk32, uint32_t qbase, int lane, uint32_t e) {
+                                            const uint32_t* pk32, uint32_t qbase, int lane, uint32_t e,
+                                            uint32_t pk_words) {
   const uint32_t off = e & 0xFFFFu, ccode = e >> 16;
   const uint32_t rep = B == 2 ? ccode * 0x55555555u : 0u - ccode;
   // bit offset of position 16c + off relative to the start of W0 (lane parity matters for b = 1)
@@ -466,6 +483,7 @@ __device__ __forceinline__ void packed_step(uint32_t (&F)[CPL], const uint32_t (
 #pragma unroll
     for (int it = 0; it < CPL; ++it) {
       const uint32_t* pw = p + it * (B == 2 ? 32 : 16);
+      SMGPU_DCHECK((uint32_t)(pw - pk32) + 1u < pk_words);
       const uint32_t w = __funnelshift_r(pw[0], pw[1], sh);
       if (B == 2) {
         const uint32_t x = ~(w ^ rep);
@@ -482,7 +500,8 @@ __device__ __forceinline__ void packed_step(uint32_t (&F)[CPL], const uint32_t (
 // Alg. 4 on the codes: r peeled steps, then the pi-ordered loop with a warp-uniform
 // exit test.  Returns per-chunk 16-bit match masks.
 template <int CPL, int B>
-__device__ __forceinline__ void packed_tile(const Pat& pt, const uint8_t* buf, uint8_t* pk, uint32_t nchunks,
+__device__ __forceinline__ void packed_tile(const Pat& pt, const uint8_t* buf, uint8_t* pk, uint32_t pk_words,
+                                            uint32_t nchunks,
                                             uint32_t code_shift, uint32_t cw0, int warp, int lane, bool edge,
                                             int32_t rlo, int32_t rhi, uint64_t* empty_bar, uint32_t* m_out) {
 #pragma unroll
@@ -490,8 +509,10 @@ __device__ __forceinline__ void packed_tile(const Pat& pt, const uint8_t* buf, u
     const uint32_t c = cw0 + it * 32u + lane;
     store_codes<B>(pk, c, pack_chunk<B>(lds128(buf + 16u * c), code_shift));
   }
-  for (uint32_t c = (uint32_t)CPL * kLanesPerTilePass + warp * 32u + lane; c < nchunks; c += kLanesPerTilePass)
+  for (uint32_t c = (uint32_t)CPL * kLanesPerTilePass + warp * 32u + lane; c < nchunks; c += kLanesPerTilePass) {
+    SMGPU_DCHECK(16u * c + 16u <= pt.lim && (c + 1u) * 2u * B <= 4u * pk_words);
     store_codes<B>(pk, c, pack_chunk<B>(lds128(buf + 16u * c), code_shift));  // halo chunks
+  }
   __syncwarp();
   if (lane == 0) mbar_arrive(empty_bar);  // the stage's bytes are no longer needed
   named_bar_sync(1, kConsumerWarps * 32);  // all codes of the tile are in place
@@ -503,17 +524,18 @@ __device__ __forceinline__ void packed_tile(const Pat& pt, const uint8_t* buf, u
     const uint32_t vm = edge ? range_mask16_rel((int32_t)(16u * (cw0 + it * 32u + lane)), rlo, rhi) : 0xFFFFu;
     F[it] = B == 2 ? spread2(vm) : vm;
     const uint32_t q = qbase + it * (B == 2 ? 32 : 16);
+    SMGPU_DCHECK(q + 1u < pk_words);
     W0[it] = pk32[q];
     W1[it] = pk32[q + 1];
   }
   uint32_t k = 0;
-  for (; k < pt.r; ++k) packed_step<CPL, B>(F, W0, W1, pk32, qbase, lane, pt.tbl[k]);  // peeled
+  for (; k < pt.r; ++k) packed_step<CPL, B>(F, W0, W1, pk32, qbase, lane, pt.tbl[k], pk_words);  // peeled
   for (; k < pt.m; ++k) {  // ordered loop with exit test, warp-uniform
     uint32_t any = 0;
 #pragma unroll
     for (int it = 0; it < CPL; ++it) any |= F[it];
     if (!__any_sync(0xFFFFFFFFu, any != 0)) break;
-    packed_step<CPL, B>(F, W0, W1, pk32, qbase, lane, pt.tbl[k]);
+    packed_step<CPL, B>(F, W0, W1, pk32, qbase, lane, pt.tbl[k], pk_words);
   }
 #pragma unroll
   for (int it = 0; it < CPL; ++it) m_out[it] = B == 2 ? gather2(F[it]) : (F[it] & 0xFFFFu);
@@ -570,7 +592,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
     if (EPI == kEpiWrite && a.tile_offsets[w + 1] == a.tile_offsets[w]) continue;
     mbar_wait(&full[s], ph);
     const uint8_t* buf = ring + (size_t)s * a.stage_stride;
-    const Pat pt{d.m, d.r, d.a1, d.bc1, d.s2, d.bc2, d.pre, P.e + d.tbl};
+    const Pat pt{d.m, d.r, d.a1, d.bc1, d.s2, d.bc2, d.pre, d.stage_len, P.e + d.tbl};
     const bool edge = ti < d.edge_lo || ti >= d.edge_hi;  // tile holds invalid alignments
     const int64_t shift = (STRAT == kFilter) ? (int64_t)d.a1 : 0;
     const int64_t x_base = (int64_t)((d.k_begin + ti) * T) - shift;  // alignment offset of u = 0
@@ -609,7 +631,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
       constexpr int B = STRAT == kPacked2 ? 2 : 1;
       uint32_t mk[CPL];
       uint8_t* pk = smem + a.pack_off + par_pk * a.pack_bytes;
-      packed_tile<CPL, B>(pt, buf, pk, d.stage_len / 16u, a.code_shift, cw0, warp, lane, edge, rlo, rhi, &empty[s], mk);
+      packed_tile<CPL, B>(pt, buf, pk, a.pack_bytes / 4u, d.stage_len / 16u, a.code_shift, cw0, warp, lane, edge, rlo, rhi, &empty[s], mk);
       par_pk ^= 1u;
       uint32_t tc = 0;
 #pragma unroll

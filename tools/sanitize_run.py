@@ -1,0 +1,44 @@
+#!/usr/bin/env python
+"""Small workload for compute-sanitizer: every strategy x epilogue, unaligned views,
+ragged ends, batches; checks results against the oracle (test infrastructure)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import oracle
+import paper_1612_01506_b200 as sm
+
+torch.cuda.set_device(0)
+print("library:", sm.load_library()._name)
+rng = np.random.default_rng(2024)
+fails = 0
+for alpha in (b"ACGT", b"\x00\x01", bytes(range(32, 127))):
+    syms = np.frombuffer(alpha, dtype=np.uint8)
+    for n in (5, 31, 4100, 70003):
+        a = syms[rng.integers(0, syms.size, n)]
+        h = oracle.hist(a)
+        for off in (0, 3, 15):
+            buf = torch.zeros(n + off, dtype=torch.uint8, device="cuda")
+            buf[off:].copy_(torch.from_numpy(a))
+            t = buf[off:]                          # the allocation ends exactly at t + n
+            pats = []
+            for m in (1, 2, 3, 17, 40):
+                if m <= n:
+                    s = int(rng.integers(0, n - m + 1))
+                    pats.append(a[s:s + m].tobytes())
+            strategies = [1, 2] + ([3] if len(alpha) <= 4 else [])
+            for strat in strategies:
+                d = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
+                sm.sm_count_batch(pats, t, d, hist=h, strategy=strat)
+                want = [oracle.naive_count(p, a) for p in pats]
+                fails += d.cpu().tolist() != want
+                cap = sum(want)
+                pos = torch.zeros(max(cap, 1), dtype=torch.int64, device="cuda")
+                d2 = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
+                sm.sm_report_batch(pats, t, pos[:cap] if cap else None, d2, hist=h, strategy=strat)
+                wp = np.concatenate([oracle.naive_report(p, a) for p in pats]) if pats else np.zeros(0)
+                fails += not np.array_equal(pos[:cap].cpu().numpy().astype(np.uint64), wp.astype(np.uint64))
+            fails += sm.sm_histogram(t).cpu().numpy().astype(np.uint64).tolist() != h.tolist()
+torch.cuda.synchronize()
+print("sanitize workload done, mismatches:", fails)
+sys.exit(1 if fails else 0)
