@@ -165,6 +165,17 @@ sm_status sm_report_batch(const uint8_t* const* p, const size_t* m, size_t P, co
                           size_t max_alignments, const uint64_t* hist, int strategy, uint64_t* pos, size_t cap,
                           uint64_t* d_counts, void* stream);
 
+/* Fixed comparison orders of PAPER.md:184-186 (Sec. 2.4), for the order ablation
+ * (the paper's N / N-freq / N-fixed columns).  Host-only; order[m] out (0-based).
+ *   SM_ORDER_IDENTITY: 0, 1, ..., m-1 (Algs. 1-2).
+ *   SM_ORDER_PI_H:     p[1], p[m], p[4], p[7], ..., p[3], p[6], ..., p[2], p[5], ...
+ *                      (1-based; stride-3 chains from 4, 3, 2, taken positions skipped).
+ *   SM_ORDER_PI_HS:    pi_h over the non-`space` positions, then the `space` positions
+ *                      ascending ("moving first all the spaces to the end").
+ * The result is a permutation usable as `order` in sm_count_async / sm_report_async. */
+typedef enum sm_order_kind { SM_ORDER_IDENTITY = 0, SM_ORDER_PI_H = 1, SM_ORDER_PI_HS = 2 } sm_order_kind;
+sm_status sm_heuristic_order(const uint8_t* p, size_t m, int kind, uint8_t space, uint32_t* order);
+
 /* Plan introspection (host-only, no GPU work): the strategy and peeling
  * factor sm_count_async would pick for (p, hist, order).  Used by tests and
  * the benchmark to label measurements. */

@@ -39,7 +39,7 @@ STRATEGY_NAMES = {1: "filter", 2: "block", 3: "packed1", 4: "packed2"}
 
 EXPORTED_SYMBOLS = (
     "sm_count", "sm_report", "sm_symbol_order", "sm_histogram", "sm_order_from_histogram",
-    "sm_count_async", "sm_count_batch", "sm_report_async", "sm_report_batch", "sm_plan", "sm_last_error", "sm_last_error_message",
+    "sm_count_async", "sm_count_batch", "sm_report_async", "sm_report_batch", "sm_heuristic_order", "sm_plan", "sm_last_error", "sm_last_error_message",
     "sm_clear_error", "sm_status_string", "sm_version", "sm_launch_count",
 )
 
@@ -87,6 +87,8 @@ def load_library(path: str = LIB_PATH):
     lib.sm_report_async.restype = ctypes.c_int
     lib.sm_report_async.argtypes = [_u8p, _sz, _u8p, _sz, _vp, _vp, ctypes.c_uint32, ctypes.c_int, _vp, _sz,
                                     _vp, _vp]
+    lib.sm_heuristic_order.restype = ctypes.c_int
+    lib.sm_heuristic_order.argtypes = [_u8p, _sz, ctypes.c_int, ctypes.c_uint8, _vp]
     lib.sm_plan.restype = ctypes.c_int
     lib.sm_plan.argtypes = [_u8p, _sz, _vp, _vp, ctypes.c_uint32, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
                             ctypes.POINTER(ctypes.c_uint32)]
@@ -311,6 +313,20 @@ def sm_report_async(p, t, pos, d_count, hist=None, order: Optional[Sequence[int]
                             _stream(stream))
     if s != SM_OK:
         _raise(s)
+
+
+SM_ORDER_IDENTITY, SM_ORDER_PI_H, SM_ORDER_PI_HS = 0, 1, 2
+
+
+def sm_heuristic_order(p, kind: int, space: int = 0x20) -> list:
+    """Fixed comparison orders of PAPER.md:184-186 (identity, pi_h, pi_hs), 0-based."""
+    lib = load_library()
+    pb, m = _pattern(p)
+    out = np.zeros(max(m, 1), dtype=np.uint32)
+    s = lib.sm_heuristic_order(pb, m, kind, space, out.ctypes.data)
+    if s != SM_OK:
+        _raise(s)
+    return out[:m].tolist()
 
 
 def sm_plan(p, hist, order=None, peel: int = 0, strategy: int = SM_STRATEGY_AUTO) -> Tuple[int, int]:

@@ -711,6 +711,40 @@ sm_status sm_report_async(const uint8_t* p, size_t m, const uint8_t* t, size_t n
   return enqueue_report(p, m, t, n, hist, order, peel, strategy, pos, cap, d_count, as_stream(stream));
 }
 
+sm_status sm_heuristic_order(const uint8_t* p, size_t m, int kind, uint8_t space, uint32_t* order) {
+  if (m == 0 || !order || (kind != SM_ORDER_IDENTITY && !p)) return fail(SM_EINVAL, "bad arguments to sm_heuristic_order");
+  if (kind == SM_ORDER_IDENTITY) {
+    for (size_t j = 0; j < m; ++j) order[j] = (uint32_t)j;
+    return SM_OK;
+  }
+  if (kind != SM_ORDER_PI_H && kind != SM_ORDER_PI_HS) return fail(SM_EINVAL, "unknown order kind");
+  // positions taking part in the pi_h traversal: all (pi_h) or the non-space ones (pi_hs)
+  std::vector<uint32_t> R;
+  for (size_t j = 0; j < m; ++j)
+    if (kind == SM_ORDER_PI_H || p[j] != space) R.push_back((uint32_t)j);
+  // pi_h over R by rank: first, last, then stride-3 chains from the
+  // 4th, 3rd, 2nd element (1-based), skipping ranks already taken (reading R18)
+  const size_t r = R.size();
+  std::vector<char> used(r + 1, 0);
+  size_t k = 0;
+  auto take = [&](size_t rank1) {  // 1-based rank
+    if (rank1 >= 1 && rank1 <= r && !used[rank1]) {
+      used[rank1] = 1;
+      order[k++] = R[rank1 - 1];
+    }
+  };
+  if (r) {
+    take(1);
+    take(r);
+    for (size_t start : {4, 3, 2})
+      for (size_t q = start; q <= r; q += 3) take(q);
+  }
+  if (kind == SM_ORDER_PI_HS)  // spaces last, ascending
+    for (size_t j = 0; j < m; ++j)
+      if (p[j] == space) order[k++] = (uint32_t)j;
+  return SM_OK;
+}
+
 sm_status sm_plan(const uint8_t* p, size_t m, const uint64_t* hist, const uint32_t* order, uint32_t peel,
                   int strategy, int* strategy_out, uint32_t* peel_out) {
   if (m == 0 || m > SM_MAX_PATTERN || !p || !hist) return fail(SM_EINVAL, "bad arguments to sm_plan");

@@ -76,3 +76,19 @@ def test_argument_errors_without_gpu(sm):
     assert lib.sm_status_string(2) == b"SM_ETRUNC"
     with pytest.raises(sm.SmError):
         sm.sm_plan(b"ab", np.ones(256), order=[1, 1])
+
+
+def test_heuristic_orders_vs_oracle_pi_h(sm):
+    for m in range(1, 300):
+        p = bytes((j * 7) % 251 for j in range(m))
+        assert sm.sm_heuristic_order(p, sm.SM_ORDER_PI_H) == oracle.pi_h(m).tolist()
+        assert sm.sm_heuristic_order(p, sm.SM_ORDER_IDENTITY) == list(range(m))
+    # pi_hs: spaces last; the rest follows pi_h over the non-space ranks
+    p = b"ab cd e  fgh"
+    o = sm.sm_heuristic_order(p, sm.SM_ORDER_PI_HS)
+    spaces = [j for j, c in enumerate(p) if c == 0x20]
+    assert o[len(o) - len(spaces):] == spaces and sorted(o) == list(range(len(p)))
+    rest = [j for j, c in enumerate(p) if c != 0x20]
+    assert o[: len(rest)] == [rest[i] for i in oracle.pi_h(len(rest)).tolist()]
+    assert sm.sm_heuristic_order(b"    ", sm.SM_ORDER_PI_HS) == [0, 1, 2, 3]
+    assert sm.sm_heuristic_order(b"ab", sm.SM_ORDER_PI_HS) == sm.sm_heuristic_order(b"ab", sm.SM_ORDER_PI_H)

@@ -392,3 +392,36 @@ def test_packed_batch_and_dense_report(sm):
     d2 = torch.zeros(10, dtype=torch.int64, device="cuda")
     sm.sm_report_batch(sub, t, pos, d2)  # AUTO -> PACKED
     assert np.array_equal(pos.cpu().numpy().astype(np.uint64), np.concatenate([oracle.naive_report(p, a) for p in sub]))
+
+
+def test_ten_thousand_random_cases_batched(sm):
+    """>= 10k (text, pattern) cases through the batched path, every strategy."""
+    rng = np.random.default_rng(10_000)
+    total = 0
+    for trial in range(24):
+        sigma = int(rng.choice([1, 2, 3, 4, 20, 96, 256]))
+        n = int(rng.choice([100, 4096, 33_333, 200_001]))
+        a = (rng.integers(0, sigma, n) + int(rng.integers(0, 256 - sigma + 1))).astype(np.uint8)
+        pats = []
+        for _ in range(450):
+            m = int(rng.choice([1, 2, 3, 4, 6, 8, 13, 24, 40, 64, 100]))
+            m = min(m, n)
+            if rng.random() < 0.8:
+                s = int(rng.integers(0, n - m + 1))
+                pats.append(a[s:s + m].tobytes())
+            else:
+                pats.append(bytes(rng.choice(np.unique(a), m)))
+        t = dev(a, int(rng.integers(0, 16)))
+        h = oracle.hist(a)
+        want = [oracle.naive_count(p, a) for p in pats]
+        strats = [0, 1, 2] + ([3] if np.unique(a).size <= 4 else [])
+        for strat in strats:
+            try:
+                d = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
+                sm.sm_count_batch(pats, t, d, hist=h, strategy=strat)
+            except sm.SmError:
+                assert strat == 3   # PACKED refuses alphabets it cannot encode
+                continue
+            assert d.cpu().tolist() == want, (trial, sigma, n, strat)
+            total += len(pats)
+    assert total >= 10_000
