@@ -228,19 +228,21 @@ __device__ __forceinline__ uint32_t filter_entry(const Pat& pt, const uint8_t* b
 
 // pi(3..m) for the survivors of pi(1), pi(2) held by the lanes of a warp (g = 0 on
 // lanes without), early exit at the first mismatch (Alg. 3's inner loop; any
-// order gives the same result).  Short patterns: each lane checks
-// its own survivors.  Long patterns: survivors are rare, so the whole warp
-// verifies one at a time, 32 consecutive positions of pi per step.
+// order gives the same result).  Each lane first checks its own
+// survivors for pi(3..min(m, kLaneVerifyMaxM)) (at most 32 serial steps, with many
+// survivors all lanes stay busy); survivors of long patterns still alive after
+// that are finished by the whole warp, one at a time, 32 positions of pi per step.
 __device__ __forceinline__ uint32_t verify_survivors(const Pat& pt, const uint8_t* buf, uint32_t c, uint32_t g,
                                                      int lane) {
-  if (pt.m <= kLaneVerifyMaxM) {
+  const uint32_t qlane = pt.m < kLaneVerifyMaxM ? pt.m : kLaneVerifyMaxM;
+  {
     uint32_t todo = g;
     const uint8_t* xb = buf + pt.pre + 16u * c - pt.a1;  // smem address of alignment u = 16c
     while (todo) {
       const uint32_t p = __ffs(todo) - 1;
       todo &= todo - 1;
       const uint8_t* xp = xb + gbit_to_alignment(p);
-      for (uint32_t q = 2; q < pt.m; ++q) {
+      for (uint32_t q = 2; q < qlane; ++q) {
         const uint32_t e = pt.tbl[q];
         SMGPU_DCHECK((uint32_t)(xp - buf) + (e & 0xFFFFu) < pt.lim);
         if (xp[e & 0xFFFFu] != (e >> 16)) {
@@ -249,8 +251,8 @@ __device__ __forceinline__ uint32_t verify_survivors(const Pat& pt, const uint8_
         }
       }
     }
-    return g;
   }
+  if (pt.m <= kLaneVerifyMaxM) return g;
   uint32_t todo = __ballot_sync(0xFFFFFFFFu, g != 0);
   while (todo) {
     const int src = __ffs(todo) - 1;
@@ -263,7 +265,7 @@ __device__ __forceinline__ uint32_t verify_survivors(const Pat& pt, const uint8_
       const uint32_t p = __ffs(gs) - 1;
       gs &= gs - 1;
       const uint8_t* xp = xb + gbit_to_alignment(p);
-      for (uint32_t q0 = 2; q0 < pt.m; q0 += 32) {
+      for (uint32_t q0 = kLaneVerifyMaxM; q0 < pt.m; q0 += 32) {
         const uint32_t q = q0 + lane;
         bool mis = false;
         if (q < pt.m) {
@@ -282,7 +284,6 @@ __device__ __forceinline__ uint32_t verify_survivors(const Pat& pt, const uint8_
   return g;
 }
 
-// Positions of one warp's chunk stream, written in ascending order (input: compressed found word).
 // IN_G: input is a compressed found word (FILTER/BLOCK), else a 16-bit mask.
 template <bool IN_G = true>
 struct WriteSink {
