@@ -316,7 +316,10 @@ void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_
     }
   L.a.npat = (uint32_t)ps.size();
   L.a.tbl_words = (uint32_t)L.e.size();
-  L.a.pack_off = (kTblOff + 127) & ~127u;
+  // reporting launches reserve the per-warp position lists
+  L.a.list_off = (kTblOff + 127) & ~127u;
+  const uint32_t list_bytes = epilogue == kEpiCount ? 0u : (uint32_t)(kConsumerWarps * kListCap * 2);
+  L.a.pack_off = (L.a.list_off + list_bytes + 127) & ~127u;
   L.a.ring_off = L.a.pack_off;
   uint32_t T = ps[0]->pl.tile;
   for (;;) {

@@ -15,6 +15,7 @@ constexpr int kGroup = 8;                                // FILTER: chunk-rows p
 constexpr int kQueueLen = 32 * kGroup;                   // FILTER: queue entries per warp
 constexpr uint32_t kLaneVerifyMaxM = 34;                 // FILTER: per-lane verification up to this m
 constexpr int kMaxBatch = 32;                            // patterns per launch
+constexpr int kListCap = 512;                            // reporting: buffered positions per warp and tile
 constexpr int kTableSmall = 256;                         // pattern-table capacities (u32 entries)
 constexpr int kTableLarge = 7168;                        // fills the 32 KiB kernel-parameter space
 constexpr int kBatchTableWords = kTableLarge;            // batching: table entries per launch
@@ -66,6 +67,7 @@ struct LaunchArgs {
   uint32_t code_shift;       // PACKED: code(x) = (x >> code_shift) & (2^b - 1), injective on the text's symbols
   uint32_t pack_off;         // PACKED: smem byte offset of the double-buffered code array
   uint32_t pack_bytes;       // PACKED: bytes of one code buffer
+  uint32_t list_off;         // reporting: smem byte offset of the per-warp position lists [W][kListCap] u16
   uint64_t* tile_counts;     // kEpiTileCount: u64[total_work] per work item (zeroed by host)
   const uint64_t* tile_offsets;  // kEpiWrite: exclusive prefix over work items, total_work + 1 entries
   uint64_t* pos;             // kEpiWrite: output positions

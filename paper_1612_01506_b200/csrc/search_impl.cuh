@@ -306,6 +306,28 @@ struct WriteSink {
   }
 };
 
+// Reporting: one warp's matches of a tile, ascending, as tile-relative alignment
+// offsets u = 16c + b (u16, T <= 32 KiB) in the warp's shared list; n counts all of
+// them even when the list (kListCap entries) overflows.
+template <bool IN_G>
+struct AppendSink {
+  uint16_t* list;
+  uint32_t n = 0;
+  __device__ __forceinline__ void operator()(uint32_t c, uint32_t g, int lane) {
+    uint32_t m16 = IN_G ? g_to_mask16(g) : g;
+    const uint32_t pc = __popc(m16);
+    const uint32_t incl = warp_incl_scan(pc, lane);
+    uint32_t idx = n + incl - pc;
+    while (m16) {
+      const uint32_t b = __ffs(m16) - 1;
+      m16 &= m16 - 1;
+      if (idx < (uint32_t)kListCap) list[idx] = (uint16_t)(16u * c + b);
+      ++idx;
+    }
+    n += __shfl_sync(0xFFFFFFFFu, incl, 31);
+  }
+};
+
 struct CountSink {
   uint32_t n = 0;
   __device__ __forceinline__ void operator()(uint32_t, uint32_t g, int) { n += __popc(g); }
@@ -542,6 +564,45 @@ __device__ __forceinline__ void packed_tile(const Pat& pt, const uint8_t* buf, u
   for (int it = 0; it < CPL; ++it) m_out[it] = B == 2 ? gather2(F[it]) : (F[it] & 0xFFFFu);
 }
 
+// Reporting: publish this warp's match count of tile w, wait for the CTA's other
+// compare warps, return the warp's first output index (tile offset + earlier warps).
+__device__ __forceinline__ uint64_t publish_and_offset(const LaunchArgs& a, uint32_t* s_wt, uint32_t par, int warp,
+                                                       int lane, uint64_t w, uint32_t wtot) {
+  if (lane == 0) s_wt[par * kConsumerWarps + warp] = wtot;
+  named_bar_sync(1, kConsumerWarps * 32);
+  uint64_t run = a.tile_offsets[w];
+  for (int wv = 0; wv < warp; ++wv) run += s_wt[par * kConsumerWarps + wv];
+  return run;
+}
+
+// Coalesced write of a warp's buffered positions (lane i writes entries i, i+32, ...).
+__device__ __forceinline__ void write_list(const LaunchArgs& a, const uint16_t* list, uint32_t cnt, uint64_t run,
+                                           int64_t pbase, int lane) {
+  for (uint32_t i = lane; i < cnt; i += 32) {
+    const uint64_t idx = run + i;
+    if (idx < a.cap) a.pos[idx] = (uint64_t)(pbase + (int64_t)list[i]);
+  }
+}
+
+// Reporting for strategies whose per-chunk results are still in registers.
+template <bool IN_G, int CPL>
+__device__ __forceinline__ void write_masks(const LaunchArgs& a, uint32_t* s_wt, uint16_t* list, uint32_t par,
+                                            int warp, int lane, uint64_t w, uint32_t cw0, int64_t x_base,
+                                            const uint32_t (&mk)[CPL]) {
+  AppendSink<IN_G> as{list};
+#pragma unroll
+  for (int it = 0; it < CPL; ++it) as(cw0 + it * 32u + lane, mk[it], lane);
+  const uint64_t run = publish_and_offset(a, s_wt, par, warp, lane, w, as.n);
+  __syncwarp();
+  if (as.n <= (uint32_t)kListCap) {
+    write_list(a, list, as.n, run, x_base - (int64_t)a.delta, lane);
+  } else {
+    WriteSink<IN_G> ws{run, x_base - (int64_t)a.delta, a.pos, a.cap};
+#pragma unroll
+    for (int it = 0; it < CPL; ++it) ws(cw0 + it * 32u + lane, mk[it], lane);
+  }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -574,6 +635,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
   }
 
   uint16_t* qc = reinterpret_cast<uint16_t*>(smem + kQueueOff) + warp * kQueueLen;
+  uint16_t* list = reinterpret_cast<uint16_t*>(smem + a.list_off) + warp * kListCap;  // reporting only
   const uint32_t T = a.tile;
   const uint32_t cw0 = (uint32_t)warp * 32u * CPL;  // first chunk of this warp
   uint32_t s = 0, ph = 0, par = 0, par_pk = 0;
@@ -617,15 +679,16 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
             atomicAdd(reinterpret_cast<unsigned long long*>(d.count_out), (unsigned long long)ws);
           }
         }
-      } else {  // two passes: this warp's total, then ranked writes
-        CountSink cs;
-        filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, cs);
-        const uint32_t wtot = __reduce_add_sync(0xFFFFFFFFu, cs.n);
-        if (lane == 0) s_wt[par * kConsumerWarps + warp] = wtot;
-        named_bar_sync(1, kConsumerWarps * 32);
-        WriteSink<> ws{a.tile_offsets[w], x_base - (int64_t)a.delta, a.pos, a.cap};
-        for (int wv = 0; wv < warp; ++wv) ws.run += s_wt[par * kConsumerWarps + wv];
-        filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, ws);
+      } else {  // buffer this warp's matches, exchange warp totals, write coalesced
+        AppendSink<true> as{list};
+        filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, as);
+        uint64_t run = publish_and_offset(a, s_wt, par, warp, lane, w, as.n);
+        if (as.n <= (uint32_t)kListCap) {
+          write_list(a, list, as.n, run, x_base - (int64_t)a.delta, lane);
+        } else {  // list overflow (very dense tile): ranked writes from a recomputation
+          WriteSink<> ws{run, x_base - (int64_t)a.delta, a.pos, a.cap};
+          filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, ws);
+        }
         par ^= 1u;
       }
     } else if (STRAT == kPacked1 || STRAT == kPacked2) {
@@ -646,13 +709,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
           atomicAdd(reinterpret_cast<unsigned long long*>(d.count_out), (unsigned long long)ws);
         }
       } else {
-        const uint32_t wtot = __reduce_add_sync(0xFFFFFFFFu, tc);
-        if (lane == 0) s_wt[par * kConsumerWarps + warp] = wtot;
-        named_bar_sync(1, kConsumerWarps * 32);
-        WriteSink<false> ws{a.tile_offsets[w], x_base - (int64_t)a.delta, a.pos, a.cap};
-        for (int wv = 0; wv < warp; ++wv) ws.run += s_wt[par * kConsumerWarps + wv];
-#pragma unroll
-        for (int it = 0; it < CPL; ++it) ws(cw0 + it * 32u + lane, mk[it], lane);
+        write_masks<false, CPL>(a, s_wt, list, par, warp, lane, w, cw0, x_base, mk);
         par ^= 1u;
       }
     } else {
@@ -670,13 +727,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
           atomicAdd(reinterpret_cast<unsigned long long*>(d.count_out), (unsigned long long)ws);
         }
       } else {
-        const uint32_t wtot = __reduce_add_sync(0xFFFFFFFFu, tc);
-        if (lane == 0) s_wt[par * kConsumerWarps + warp] = wtot;
-        named_bar_sync(1, kConsumerWarps * 32);
-        WriteSink<> ws{a.tile_offsets[w], x_base - (int64_t)a.delta, a.pos, a.cap};
-        for (int wv = 0; wv < warp; ++wv) ws.run += s_wt[par * kConsumerWarps + wv];
-#pragma unroll
-        for (int it = 0; it < CPL; ++it) ws(cw0 + it * 32u + lane, g[it], lane);
+        write_masks<true, CPL>(a, s_wt, list, par, warp, lane, w, cw0, x_base, g);
         par ^= 1u;
       }
     }
