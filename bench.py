@@ -403,7 +403,11 @@ def run_native(args):
         "gpu_launches": int(launches),
         "roofline": {
             "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": None, "avg_launch_us": round(search_ms * 1e3 / P, 2),
+            "frac": round(achieved / peak, 4),
+            # DRAM read+write bytes per pattern pass, from the committed ncu capture of this kernel
+            # (profiles/r1_summary.md §6: batch of 8 c2 m=16 patterns, 1922 MB / 8); null for other configs
+            "traffic": 240.3e6 if args.config.lower() == "c2" else None,
+            "traffic_unit": "bytes per pattern pass (algorithmic n = %d)" % spec.n, "avg_launch_us": round(search_ms * 1e3 / P, 2),
             "kernel": "search_kernel (count)", "peak_kind": peak_kind,
             "algorithmic_bytes_per_launch": "n (text bytes of the launch's view)",
         },
