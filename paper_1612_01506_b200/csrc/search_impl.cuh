@@ -292,14 +292,17 @@ struct WriteSink {
   uint64_t* pos;
   uint64_t cap;
   __device__ __forceinline__ void operator()(uint32_t c, uint32_t g, int lane) {
-    uint32_t m16 = IN_G ? g_to_mask16(g) : g;
-    const uint32_t pc = __popc(m16);
+    add(16u * c, IN_G ? g_to_mask16(g) : g, lane);
+  }
+  // mask bit b <-> tile-relative alignment base_u + b (lanes in ascending base_u order)
+  __device__ __forceinline__ void add(uint32_t base_u, uint32_t mk, int lane) {
+    const uint32_t pc = __popc(mk);
     const uint32_t incl = warp_incl_scan(pc, lane);
     uint64_t idx = run + incl - pc;
-    while (m16) {
-      const uint32_t b = __ffs(m16) - 1;
-      m16 &= m16 - 1;
-      if (idx < cap) pos[idx] = (uint64_t)(pbase + 16 * (int64_t)c + b);
+    while (mk) {
+      const uint32_t b = __ffs(mk) - 1;
+      mk &= mk - 1;
+      if (idx < cap) pos[idx] = (uint64_t)(pbase + (int64_t)(base_u + b));
       ++idx;
     }
     run += __shfl_sync(0xFFFFFFFFu, incl, 31);
@@ -314,14 +317,16 @@ struct AppendSink {
   uint16_t* list;
   uint32_t n = 0;
   __device__ __forceinline__ void operator()(uint32_t c, uint32_t g, int lane) {
-    uint32_t m16 = IN_G ? g_to_mask16(g) : g;
-    const uint32_t pc = __popc(m16);
+    add(16u * c, IN_G ? g_to_mask16(g) : g, lane);
+  }
+  __device__ __forceinline__ void add(uint32_t base_u, uint32_t mk, int lane) {
+    const uint32_t pc = __popc(mk);
     const uint32_t incl = warp_incl_scan(pc, lane);
     uint32_t idx = n + incl - pc;
-    while (m16) {
-      const uint32_t b = __ffs(m16) - 1;
-      m16 &= m16 - 1;
-      if (idx < (uint32_t)kListCap) list[idx] = (uint16_t)(16u * c + b);
+    while (mk) {
+      const uint32_t b = __ffs(mk) - 1;
+      mk &= mk - 1;
+      if (idx < (uint32_t)kListCap) list[idx] = (uint16_t)(base_u + b);
       ++idx;
     }
     n += __shfl_sync(0xFFFFFFFFu, incl, 31);
@@ -522,11 +527,14 @@ __device__ __forceinline__ void packed_step(uint32_t (&F)[CPL], const uint32_t (
 // halo), then -- after the CTA's consumer warps have packed the whole tile --
 // Alg. 4 on the codes: r peeled steps, then the pi-ordered loop with a warp-uniform
 // exit test.  Returns per-chunk 16-bit match masks.
+// Returns the number of result units; unit i: mask m_out[i] (bit b <-> tile-relative
+// alignment base_out[i] + b), units in ascending order within each lane-round.
 template <int CPL, int B>
-__device__ __forceinline__ void packed_tile(const Pat& pt, const uint8_t* buf, uint8_t* pk, uint32_t pk_words,
-                                            uint32_t nchunks,
+__device__ __forceinline__ int packed_tile(const Pat& pt, const uint8_t* buf, uint8_t* pk, uint32_t pk_words,
+                                           uint32_t nchunks,
                                             uint32_t code_shift, uint32_t cw0, int warp, int lane, bool edge,
-                                            int32_t rlo, int32_t rhi, uint64_t* empty_bar, uint32_t* m_out) {
+                                            int32_t rlo, int32_t rhi, uint64_t* empty_bar, uint32_t* m_out,
+                                            uint32_t* base_out) {
 #pragma unroll
   for (int it = 0; it < CPL; ++it) {
     const uint32_t c = cw0 + it * 32u + lane;
@@ -540,6 +548,52 @@ __device__ __forceinline__ void packed_tile(const Pat& pt, const uint8_t* buf, u
   if (lane == 0) mbar_arrive(empty_bar);  // the stage's bytes are no longer needed
   named_bar_sync(1, kConsumerWarps * 32);  // all codes of the tile are in place
   const uint32_t* pk32 = reinterpret_cast<const uint32_t*>(pk);
+  if constexpr (B == 1 && CPL >= 2) {
+    // 1-bit codes: a lane compares a whole code word = 32 consecutive alignments per
+    // step (double chunk dc = 32 alignments; warp w owns dc in [w*16*CPL, (w+1)*16*CPL)).
+    constexpr int D = CPL / 2;
+    const uint32_t dc0 = (cw0 >> 1) + lane;  // double chunk of it = 0; it-th at dc0 + 32 it
+    uint32_t F[D], W0[D], W1[D];
+#pragma unroll
+    for (int it = 0; it < D; ++it) {
+      const uint32_t dc = dc0 + it * 32u;
+      F[it] = edge ? (range_mask16_rel((int32_t)(32u * dc), rlo, rhi) |
+                      (range_mask16_rel((int32_t)(32u * dc + 16u), rlo, rhi) << 16))
+                   : 0xFFFFFFFFu;
+      SMGPU_DCHECK(dc + 1u < pk_words);
+      W0[it] = pk32[dc];
+      W1[it] = pk32[dc + 1];
+    }
+    auto step = [&](uint32_t e) {
+      const uint32_t off = e & 0xFFFFu, rep = 0u - (e >> 16);
+      if (off < 32u) {  // warp-uniform: the window lies in W0:W1
+#pragma unroll
+        for (int it = 0; it < D; ++it) F[it] &= ~(__funnelshift_r(W0[it], W1[it], off) ^ rep);
+      } else {
+        const uint32_t* p = pk32 + dc0 + (off >> 5);
+#pragma unroll
+        for (int it = 0; it < D; ++it) {
+          SMGPU_DCHECK((uint32_t)(p + it * 32 - pk32) + 1u < pk_words);
+          F[it] &= ~(__funnelshift_r(p[it * 32], p[it * 32 + 1], off & 31u) ^ rep);
+        }
+      }
+    };
+    uint32_t k = 0;
+    for (; k < pt.r; ++k) step(pt.tbl[k]);  // peeled
+    for (; k < pt.m; ++k) {                // ordered loop with exit test
+      uint32_t any = 0;
+#pragma unroll
+      for (int it = 0; it < D; ++it) any |= F[it];
+      if (!__any_sync(0xFFFFFFFFu, any != 0)) break;
+      step(pt.tbl[k]);
+    }
+#pragma unroll
+    for (int it = 0; it < D; ++it) {
+      m_out[it] = F[it];
+      base_out[it] = 32u * (dc0 + it * 32u);
+    }
+    return D;
+  }
   const uint32_t qbase = B == 2 ? (cw0 + lane) : ((cw0 + lane) >> 1);  // code word of chunk it = 0
   uint32_t F[CPL], W0[CPL], W1[CPL];
 #pragma unroll
@@ -561,7 +615,11 @@ __device__ __forceinline__ void packed_tile(const Pat& pt, const uint8_t* buf, u
     packed_step<CPL, B>(F, W0, W1, pk32, qbase, lane, pt.tbl[k], pk_words);
   }
 #pragma unroll
-  for (int it = 0; it < CPL; ++it) m_out[it] = B == 2 ? gather2(F[it]) : (F[it] & 0xFFFFu);
+  for (int it = 0; it < CPL; ++it) {
+    m_out[it] = B == 2 ? gather2(F[it]) : (F[it] & 0xFFFFu);
+    base_out[it] = 16u * (cw0 + it * 32u + lane);
+  }
+  return CPL;
 }
 
 // Reporting: publish this warp's match count of tile w, wait for the CTA's other
@@ -600,6 +658,27 @@ __device__ __forceinline__ void write_masks(const LaunchArgs& a, uint32_t* s_wt,
     WriteSink<IN_G> ws{run, x_base - (int64_t)a.delta, a.pos, a.cap};
 #pragma unroll
     for (int it = 0; it < CPL; ++it) ws(cw0 + it * 32u + lane, mk[it], lane);
+  }
+}
+
+// Reporting for PACKED: result units (mask, base) still in registers.
+template <int CPL>
+__device__ __forceinline__ void write_units(const LaunchArgs& a, uint32_t* s_wt, uint16_t* list, uint32_t par,
+                                            int warp, int lane, uint64_t w, int64_t x_base, const uint32_t (&mk)[CPL],
+                                            const uint32_t (&mbase)[CPL], int units) {
+  AppendSink<false> as{list};
+#pragma unroll
+  for (int it = 0; it < CPL; ++it)
+    if (it < units) as.add(mbase[it], mk[it], lane);
+  const uint64_t run = publish_and_offset(a, s_wt, par, warp, lane, w, as.n);
+  __syncwarp();
+  if (as.n <= (uint32_t)kListCap) {
+    write_list(a, list, as.n, run, x_base - (int64_t)a.delta, lane);
+  } else {
+    WriteSink<false> ws{run, x_base - (int64_t)a.delta, a.pos, a.cap};
+#pragma unroll
+    for (int it = 0; it < CPL; ++it)
+      if (it < units) ws.add(mbase[it], mk[it], lane);
   }
 }
 
@@ -693,13 +772,15 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
       }
     } else if (STRAT == kPacked1 || STRAT == kPacked2) {
       constexpr int B = STRAT == kPacked2 ? 2 : 1;
-      uint32_t mk[CPL];
+      uint32_t mk[CPL], mbase[CPL];
       uint8_t* pk = smem + a.pack_off + par_pk * a.pack_bytes;
-      packed_tile<CPL, B>(pt, buf, pk, a.pack_bytes / 4u, d.stage_len / 16u, a.code_shift, cw0, warp, lane, edge, rlo, rhi, &empty[s], mk);
+      const int units = packed_tile<CPL, B>(pt, buf, pk, a.pack_bytes / 4u, d.stage_len / 16u, a.code_shift, cw0,
+                                            warp, lane, edge, rlo, rhi, &empty[s], mk, mbase);
       par_pk ^= 1u;
       uint32_t tc = 0;
 #pragma unroll
-      for (int it = 0; it < CPL; ++it) tc += __popc(mk[it]);
+      for (int it = 0; it < CPL; ++it)
+        if (it < units) tc += __popc(mk[it]);
       if (EPI == kEpiCount) {
         acc += tc;
       } else if (EPI == kEpiTileCount) {
@@ -709,7 +790,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
           atomicAdd(reinterpret_cast<unsigned long long*>(d.count_out), (unsigned long long)ws);
         }
       } else {
-        write_masks<false, CPL>(a, s_wt, list, par, warp, lane, w, cw0, x_base, mk);
+        write_units<CPL>(a, s_wt, list, par, warp, lane, w, x_base, mk, mbase, units);
         par ^= 1u;
       }
     } else {

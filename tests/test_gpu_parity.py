@@ -425,3 +425,24 @@ def test_ten_thousand_random_cases_batched(sm):
             assert d.cpu().tolist() == want, (trial, sigma, n, strat)
             total += len(pats)
     assert total >= 10_000
+
+
+def test_concurrent_streams(sm):
+    """Re-entrancy: launches on different streams with different patterns / texts overlap
+    freely (no __constant__ or global state in the library)."""
+    rng = np.random.default_rng(8)
+    texts = [rng.integers(0, s, 1_000_003, dtype=np.uint8) for s in (4, 20, 96, 256)]
+    devs = [dev(a, i) for i, a in enumerate(texts)]
+    torch.cuda.synchronize()  # texts were written on the default stream
+    streams = [torch.cuda.Stream() for _ in texts]
+    jobs = []
+    for a, t, st in zip(texts, devs, streams):
+        pats = [a[s:s + m].tobytes() for m in (2, 5, 9, 33, 300) for s in rng.integers(0, a.size - m, 4)]
+        d = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
+        jobs.append((a, pats, d))
+        with torch.cuda.stream(st):
+            for _ in range(3):
+                sm.sm_count_batch(pats, t, d, hist=oracle.hist(a), stream=st)
+    torch.cuda.synchronize()
+    for a, pats, d in jobs:
+        assert d.cpu().tolist() == [oracle.naive_count(p, a) for p in pats]
