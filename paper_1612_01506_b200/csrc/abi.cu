@@ -472,26 +472,38 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
     plans.push_back(std::move(q));
   }
   if (plans.empty()) return SM_OK;
-  // launches over consecutive runs (same strategy, batch limits), in pattern order
+  // launches grouped by strategy (batch limits as for counting); every pattern keeps
+  // a fixed slot range [item_base, item_base + ntiles) of the per-tile arrays in the
+  // caller's order, so one scan gives the concatenated, pattern-ordered output layout
   std::vector<HostLaunch> Ls;
-  {
+  for (int strat : {(int)kFilter, (int)kBlock, (int)kPacked1, (int)kPacked2}) {
     std::vector<const Planned*> run;
     size_t words = 0;
-    for (size_t i = 0; i <= plans.size(); ++i) {
-      const bool end = i == plans.size();
-      if (!run.empty() && (end || plans[i].pl.strategy != run[0]->pl.strategy || run.size() == (size_t)kMaxBatch ||
-                           words + plans[i].m > (size_t)kBatchTableWords)) {
-        Ls.emplace_back();
-        build_launch(run, t, n, lim, kEpiTileCount, Ls.back());
-        run.clear();
-        words = 0;
-      }
-      if (!end) {
-        run.push_back(&plans[i]);
-        words += plans[i].m;
-      }
+    auto flush = [&]() {
+      if (run.empty()) return;
+      Ls.emplace_back();
+      build_launch(run, t, n, lim, kEpiTileCount, Ls.back());
+      run.clear();
+      words = 0;
+    };
+    for (const Planned& q : plans) {
+      if (q.pl.strategy != strat) continue;
+      if (run.size() == (size_t)kMaxBatch || words + q.m > (size_t)kBatchTableWords) flush();
+      run.push_back(&q);
+      words += q.m;
     }
+    flush();
   }
+  // item bases in pattern order (a descriptor's pattern index = its count_out - d_counts)
+  std::vector<PatDesc*> slot(P, nullptr);
+  for (HostLaunch& L : Ls)
+    for (PatDesc& d : L.d) slot[(size_t)(d.count_out - d_counts)] = &d;
+  uint64_t item = 0;
+  for (size_t i = 0; i < P; ++i)
+    if (slot[i]) {
+      slot[i]->item_base = item;
+      item += slot[i]->ntiles;
+    }
   uint64_t total_work = 0;
   for (const HostLaunch& L : Ls) total_work += L.a.total_work;
   const uint64_t nt1 = total_work + 1;
@@ -505,30 +517,26 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
   uint64_t* offsets = reinterpret_cast<uint64_t*>(scratch + off_bytes);
   void* temp = scratch + 2 * off_bytes;
   cudaError_t e = cudaMemsetAsync(counts, 0, nt1 * 8, st);
-  uint64_t wb = 0;
   for (HostLaunch& L : Ls) {  // pass 1
     if (e != cudaSuccess) break;
-    L.a.tile_counts = counts + wb;
+    L.a.tile_counts = counts;
     e = launch_search(L, st);
     if (e == cudaSuccess) ++g_launches;
-    wb += L.a.total_work;
   }
   if (e == cudaSuccess) {
     e = exclusive_scan_u64(counts, offsets, nt1, temp, &temp_bytes, st);
     if (e == cudaSuccess) g_launches += 1;
   }
-  wb = 0;
   if (cap > 0) {
     for (HostLaunch& L : Ls) {  // pass 2
       if (e != cudaSuccess) break;
       L.epilogue = kEpiWrite;
       L.a.tile_counts = nullptr;
-      L.a.tile_offsets = offsets + wb;
+      L.a.tile_offsets = offsets;
       L.a.pos = pos;
       L.a.cap = cap;
       e = launch_search(L, st);
       if (e == cudaSuccess) ++g_launches;
-      wb += L.a.total_work;
     }
   }
   cudaFreeAsync(scratch, st);

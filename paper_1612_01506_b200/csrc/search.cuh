@@ -41,6 +41,7 @@ struct PatDesc {
   uint64_t edge_lo;    // tiles ti < edge_lo start before the first alignment
   uint64_t edge_hi;    // tiles ti >= edge_hi end after the last alignment
   uint64_t* count_out; // kEpiCount / kEpiTileCount: device u64 (accumulated with atomics; zeroed by host)
+  uint64_t item_base;  // reporting: index of this pattern's first tile in tile_counts / tile_offsets
   uint32_t m;
   uint32_t r;          // peeling factor (BLOCK), 1 <= r <= m
   uint32_t a1;         // pattern offset of pi(1) (FILTER)
@@ -68,8 +69,8 @@ struct LaunchArgs {
   uint32_t pack_off;         // PACKED: smem byte offset of the double-buffered code array
   uint32_t pack_bytes;       // PACKED: bytes of one code buffer
   uint32_t list_off;         // reporting: smem byte offset of the per-warp position lists [W][kListCap] u16
-  uint64_t* tile_counts;     // kEpiTileCount: u64[total_work] per work item (zeroed by host)
-  const uint64_t* tile_offsets;  // kEpiWrite: exclusive prefix over work items, total_work + 1 entries
+  uint64_t* tile_counts;     // kEpiTileCount: u64 per (pattern, tile), at item_base + ti (zeroed by host)
+  const uint64_t* tile_offsets;  // kEpiWrite: exclusive prefix of tile_counts (patterns in caller order)
   uint64_t* pos;             // kEpiWrite: output positions
   uint64_t cap;              // kEpiWrite: capacity of pos
 };

@@ -152,7 +152,7 @@ __device__ void produce(const LaunchParams<CAP>& P, uint8_t* ring, uint64_t* ful
     while (w >= P.d[k].work_end) ++k;
     const PatDesc& d = P.d[k];
     const uint64_t ti = w - (d.work_end - d.ntiles);
-    if (EPI == kEpiWrite && a.tile_offsets[w + 1] == a.tile_offsets[w]) continue;
+    if (EPI == kEpiWrite && a.tile_offsets[d.item_base + ti + 1] == a.tile_offsets[d.item_base + ti]) continue;
     if (wrapped) mbar_wait_sleep(&empty[s], ph ^ 1u);  // consumers released this stage's previous use
     uint8_t* buf = ring + (size_t)s * a.stage_stride;
     const int64_t lo = (int64_t)((d.k_begin + ti) * a.tile) - (int64_t)d.pre;
@@ -628,7 +628,7 @@ __device__ __forceinline__ uint64_t publish_and_offset(const LaunchArgs& a, uint
                                                        int lane, uint64_t w, uint32_t wtot) {
   if (lane == 0) s_wt[par * kConsumerWarps + warp] = wtot;
   named_bar_sync(1, kConsumerWarps * 32);
-  uint64_t run = a.tile_offsets[w];
+  uint64_t run = a.tile_offsets[w];  // w = item index (d.item_base + ti) here
   for (int wv = 0; wv < warp; ++wv) run += s_wt[par * kConsumerWarps + wv];
   return run;
 }
@@ -731,7 +731,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
     }
     const PatDesc& d = P.d[k];
     const uint64_t ti = w - (d.work_end - d.ntiles);
-    if (EPI == kEpiWrite && a.tile_offsets[w + 1] == a.tile_offsets[w]) continue;
+    if (EPI == kEpiWrite && a.tile_offsets[d.item_base + ti + 1] == a.tile_offsets[d.item_base + ti]) continue;
     mbar_wait(&full[s], ph);
     const uint8_t* buf = ring + (size_t)s * a.stage_stride;
     const Pat pt{d.m, d.r, d.a1, d.bc1, d.s2, d.bc2, d.pre, d.stage_len, P.e + d.tbl};
@@ -754,14 +754,14 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
         } else {
           const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, cs.n);
           if (lane == 0 && ws) {
-            atomicAdd(reinterpret_cast<unsigned long long*>(&a.tile_counts[w]), (unsigned long long)ws);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&a.tile_counts[d.item_base + ti]), (unsigned long long)ws);
             atomicAdd(reinterpret_cast<unsigned long long*>(d.count_out), (unsigned long long)ws);
           }
         }
       } else {  // buffer this warp's matches, exchange warp totals, write coalesced
         AppendSink<true> as{list};
         filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, as);
-        uint64_t run = publish_and_offset(a, s_wt, par, warp, lane, w, as.n);
+        uint64_t run = publish_and_offset(a, s_wt, par, warp, lane, d.item_base + ti, as.n);
         if (as.n <= (uint32_t)kListCap) {
           write_list(a, list, as.n, run, x_base - (int64_t)a.delta, lane);
         } else {  // list overflow (very dense tile): ranked writes from a recomputation
@@ -786,11 +786,11 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
       } else if (EPI == kEpiTileCount) {
         const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, tc);
         if (lane == 0 && ws) {
-          atomicAdd(reinterpret_cast<unsigned long long*>(&a.tile_counts[w]), (unsigned long long)ws);
+          atomicAdd(reinterpret_cast<unsigned long long*>(&a.tile_counts[d.item_base + ti]), (unsigned long long)ws);
           atomicAdd(reinterpret_cast<unsigned long long*>(d.count_out), (unsigned long long)ws);
         }
       } else {
-        write_units<CPL>(a, s_wt, list, par, warp, lane, w, x_base, mk, mbase, units);
+        write_units<CPL>(a, s_wt, list, par, warp, lane, d.item_base + ti, x_base, mk, mbase, units);
         par ^= 1u;
       }
     } else {
@@ -804,11 +804,11 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
       } else if (EPI == kEpiTileCount) {
         const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, tc);
         if (lane == 0 && ws) {
-          atomicAdd(reinterpret_cast<unsigned long long*>(&a.tile_counts[w]), (unsigned long long)ws);
+          atomicAdd(reinterpret_cast<unsigned long long*>(&a.tile_counts[d.item_base + ti]), (unsigned long long)ws);
           atomicAdd(reinterpret_cast<unsigned long long*>(d.count_out), (unsigned long long)ws);
         }
       } else {
-        write_masks<true, CPL>(a, s_wt, list, par, warp, lane, w, cw0, x_base, g);
+        write_masks<true, CPL>(a, s_wt, list, par, warp, lane, d.item_base + ti, cw0, x_base, g);
         par ^= 1u;
       }
     }
