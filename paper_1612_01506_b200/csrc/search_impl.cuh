@@ -136,23 +136,66 @@ struct Pat {
 };
 
 // ---------------------------------------------------------------------------
+// This CTA's work items w = blockIdx.x + i * gridDim.x, in order.  For the write
+// epilogue (reporting pass 2) items of tiles without matches are skipped; a warp
+// probes 32 upcoming items at once (one load per lane + a ballot) instead of one
+// dependent load per item.  Every lane of the calling warp must call advance().
+// ---------------------------------------------------------------------------
+template <int EPI, int CAP>
+struct WorkIter {
+  uint64_t next = blockIdx.x;  // next unprobed item
+  uint64_t base = 0;           // first item of the current probe
+  uint32_t mask = 0;           // non-empty items of the current probe not yet returned
+  __device__ __forceinline__ bool advance(const LaunchParams<CAP>& P, int lane, uint64_t& w) {
+    const uint64_t total = P.a.total_work, grid = gridDim.x;
+    if (EPI != kEpiWrite) {
+      if (next >= total) return false;
+      w = next;
+      next += grid;
+      return true;
+    }
+    while (mask == 0) {
+      if (next >= total) return false;
+      base = next;
+      const uint64_t wj = base + (uint64_t)lane * grid;
+      bool nonempty = false;
+      if (wj < total) {
+        uint32_t kk = 0;
+        while (wj >= P.d[kk].work_end) ++kk;
+        const PatDesc& d = P.d[kk];
+        const uint64_t item = d.item_base + wj - (d.work_end - d.ntiles);
+        nonempty = P.a.tile_offsets[item + 1] != P.a.tile_offsets[item];
+      }
+      mask = __ballot_sync(0xFFFFFFFFu, nonempty);
+      next = base + 32 * grid;
+    }
+    const uint32_t j = __ffs(mask) - 1;
+    mask &= mask - 1;
+    w = base + (uint64_t)j * grid;
+    return true;
+  }
+};
+
+// ---------------------------------------------------------------------------
 // TMA producer (one thread): for every work item (pattern, tile) of this CTA,
 // wait for a free stage, load the ragged 16-B ends of t byte-wise, then one
 // cp.async.bulk for the aligned interior, completion counted on full[s].
 // ---------------------------------------------------------------------------
 template <int EPI, int CAP>
-__device__ void produce(const LaunchParams<CAP>& P, uint8_t* ring, uint64_t* full, uint64_t* empty) {
+__device__ void produce(const LaunchParams<CAP>& P, uint8_t* ring, uint64_t* full, uint64_t* empty, int lane) {
   const LaunchArgs& a = P.a;
   const uint64_t pol = l2_policy_evict_first();
   const int64_t tlo = (int64_t)a.delta, thi = (int64_t)(a.delta + a.n);
   uint32_t s = 0, ph = 0;  // stage and its use parity
   bool wrapped = false;
   uint32_t k = 0;
-  for (uint64_t w = blockIdx.x; w < a.total_work; w += gridDim.x) {
+  WorkIter<EPI, CAP> items;
+  uint64_t w;
+  while (items.advance(P, lane, w)) {
     while (w >= P.d[k].work_end) ++k;
+    if (lane != 0) continue;  // lane 0 issues the copies; the warp only probes work items
     const PatDesc& d = P.d[k];
     const uint64_t ti = w - (d.work_end - d.ntiles);
-    if (EPI == kEpiWrite && a.tile_offsets[d.item_base + ti + 1] == a.tile_offsets[d.item_base + ti]) continue;
     if (wrapped) mbar_wait_sleep(&empty[s], ph ^ 1u);  // consumers released this stage's previous use
     uint8_t* buf = ring + (size_t)s * a.stage_stride;
     const int64_t lo = (int64_t)((d.k_begin + ti) * a.tile) - (int64_t)d.pre;
@@ -709,7 +752,8 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
   __syncthreads();
 
   if (warp == kConsumerWarps) {
-    if (lane == 0) produce<EPI>(P, ring, full, empty);
+    if (EPI == kEpiWrite) produce<EPI>(P, ring, full, empty, lane);  // the warp probes work items
+    else if (lane == 0) produce<EPI>(P, ring, full, empty, lane);
     return;
   }
 
@@ -720,7 +764,9 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
   uint32_t s = 0, ph = 0, par = 0, par_pk = 0;
   uint32_t k = 0;
   uint32_t acc = 0;  // kEpiCount: this lane's matches of pattern k so far
-  for (uint64_t w = blockIdx.x; w < a.total_work; w += gridDim.x) {
+  WorkIter<EPI, CAP> items;
+  uint64_t w;
+  while (items.advance(P, lane, w)) {
     while (w >= P.d[k].work_end) {
       if (EPI == kEpiCount) {  // flush pattern k (warp-uniform)
         const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, acc);
@@ -731,7 +777,6 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
     }
     const PatDesc& d = P.d[k];
     const uint64_t ti = w - (d.work_end - d.ntiles);
-    if (EPI == kEpiWrite && a.tile_offsets[d.item_base + ti + 1] == a.tile_offsets[d.item_base + ti]) continue;
     mbar_wait(&full[s], ph);
     const uint8_t* buf = ring + (size_t)s * a.stage_stride;
     const Pat pt{d.m, d.r, d.a1, d.bc1, d.s2, d.bc2, d.pre, d.stage_len, P.e + d.tbl};
