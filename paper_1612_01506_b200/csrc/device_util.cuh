@@ -142,9 +142,6 @@ __device__ __forceinline__ uint32_t eq_flags_raw(uint32_t w, uint32_t bc) {
   uint32_t t = (y & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;  // bit7 set iff low 7 bits nonzero
   return ~(t | y);                              // bit7 set iff y byte == 0
 }
-__device__ __forceinline__ uint32_t eq_flags(uint32_t w, uint32_t bc) {
-  return eq_flags_raw(w, bc) & 0x80808080u;
-}
 // "any byte equal" test term (exact as a whole-word predicate; per-byte bits may
 // include false positives above a true match, so it is only ever OR-reduced)
 __device__ __forceinline__ uint32_t any_eq_term(uint32_t w, uint32_t bc) {
@@ -152,10 +149,6 @@ __device__ __forceinline__ uint32_t any_eq_term(uint32_t w, uint32_t bc) {
   return (y - 0x01010101u) & ~y;
 }
 
-// 0x80-per-byte flags of one word -> 4-bit mask (bit b <-> byte b)
-__device__ __forceinline__ uint32_t flags_to_nibble(uint32_t f) {
-  return (((f >> 7) & 0x01010101u) * 0x00204081u) >> 21 & 0xFu;
-}
 // 4-bit mask -> 0x80-per-byte flags
 __device__ __forceinline__ uint32_t nibble_to_flags(uint32_t nib) {
   return ((nib * 0x00204081u) & 0x01010101u) << 7;

@@ -7,10 +7,8 @@ namespace smgpu {
 
 constexpr int kConsumerWarps = 8;                        // warps comparing text
 constexpr int kThreads = (kConsumerWarps + 1) * 32;      // + 1 TMA producer warp
-constexpr int kChunk = 16;                               // alignments per lane-chunk
 constexpr int kLanesPerTilePass = kConsumerWarps * 32;   // lanes sharing a tile
 constexpr int kMaxStages = 8;
-constexpr int kMaxCPL = 8;                               // chunks per lane per tile (tile <= 32 KiB)
 constexpr int kGroup = 8;                                // FILTER: chunk-rows per queue fill
 constexpr int kQueueLen = 32 * kGroup;                   // FILTER: queue entries per warp
 constexpr uint32_t kLaneVerifyMaxM = 34;                 // FILTER: per-lane verification up to this m

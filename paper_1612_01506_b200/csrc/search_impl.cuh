@@ -1,25 +1,25 @@
-// search_impl.cuh -- the hot path: exact occurrence counting / reporting of a
-// pattern in a device-resident byte text, pattern symbols compared rarest-first
+// search_impl.cuh -- the hot path: exact occurrence counting / reporting of
+// patterns in a device-resident byte text, pattern symbols compared rarest-first
 // with peeled first comparisons (Algs. 3-4), B200-native.
 //
-// Persistent CTAs (several per SM): warp 8 is the TMA producer, warps 0..7 compare.
-//   * A3 staging (PAPER.md:101-106 loads 16/32 unaligned bytes; here): tiles of
-//     T text bytes plus the pattern's halo are copied HBM -> shared memory with
+// Persistent CTAs (2 per SM): warp 8 is the TMA producer, warps 0..7 compare.
+// A launch runs a batch of patterns; each pattern is a full pass over the text.
+//   * A3 staging (the paper loads 16/32 unaligned bytes): tiles
+//     of T = 32 KiB plus the pattern's halo are copied HBM -> shared memory with
 //     1-D TMA bulk copies (cp.async.bulk, 16-B granules, L2 evict-first) into a
-//     ring of mbarrier-guarded stages.  Ragged 16-B ends of the text are loaded
-//     byte-wise by the producer so nothing outside t[0..n) is read.
-//   * The SIMDcompare primitive becomes a packed-byte compare:
-//     each lane owns chunks of 16 consecutive alignments held as 4 x u32 words
-//     with one flag bit (0x80) per alignment.
-//   * FILTER strategy: the first comparison pi(1) -- the rarest symbol, where the
-//     paper's frequency order pays most -- runs over the chunk
-//     with aligned 16-B shared loads; each surviving alignment continues with
-//     pi(2..m) and early exit (Alg. 3's inner loop at alpha = 1).
-//   * BLOCK strategy: Alg. 4: r peeled comparisons without a
-//     test, then the pi-ordered loop with a warp-uniform exit
-//     test (__any_sync) over all alignments the warp holds.
-//   * A6: popcount -> warp reduce -> one u64 atomic per warp.
-//   * A8: reporting writes ascending positions from a per-tile exclusive prefix.
+//     3-stage ring of mbarrier-guarded buffers.  Ragged 16-B ends of the text are
+//     loaded byte-wise by the producer, so nothing outside t[0..n) is read.
+//   * SIMDcompare becomes a packed-byte compare: a lane owns
+//     chunks of 16 consecutive alignments held as 4 x u32 words, one flag bit
+//     (0x80) per alignment -- the paper's `found`.
+//   * FILTER: pi(1) (the rarest symbol) is tested over 16-byte
+//     chunks; flagged chunks are ballot-compacted, then pi(1), pi(2) compared
+//     exactly (peeling r = 2) and pi(3..m) verified per survivor with early exit.
+//   * BLOCK: Alg. 4 as written: r peeled compares without a test,
+//     then the pi-ordered loop with a warp-uniform exit test (__any_sync).
+//   * PACKED: BLOCK on 1- or 2-bit codes of the text bytes (small alphabets).
+//   * A6: popcount -> warp reduce -> one u64 atomic per warp and pattern.
+//   * A8: reporting writes ascending positions from a per-(pattern, tile) exclusive prefix.
 #pragma once
 #include "device_util.cuh"
 #include "launch.h"
@@ -44,37 +44,11 @@ struct Found4 {
   uint32_t f0, f1, f2, f3;
 };
 
-// 16 bytes starting at smem address base16 + sel (base16 16-B aligned, sel in 0..15
-// warp-uniform): two conflict-free LDS.128 + funnel shifts.  This is SIMDcompare's
-// unaligned load (PAPER.md:101 _mm_loadu_si128) on shared memory.
-__device__ __forceinline__ uint4 load_window16(const uint8_t* base16, uint32_t sel) {
-  const uint4 lo = lds128(base16);
-  const uint4 hi = lds128(base16 + 16);
-  const uint32_t sh = (sel & 3u) * 8u;
-  uint4 w;
-  switch ((sel >> 2) & 3u) {
-    case 0:
-      w.x = byte_window(lo.x, lo.y, sh); w.y = byte_window(lo.y, lo.z, sh);
-      w.z = byte_window(lo.z, lo.w, sh); w.w = byte_window(lo.w, hi.x, sh);
-      break;
-    case 1:
-      w.x = byte_window(lo.y, lo.z, sh); w.y = byte_window(lo.z, lo.w, sh);
-      w.z = byte_window(lo.w, hi.x, sh); w.w = byte_window(hi.x, hi.y, sh);
-      break;
-    case 2:
-      w.x = byte_window(lo.z, lo.w, sh); w.y = byte_window(lo.w, hi.x, sh);
-      w.z = byte_window(hi.x, hi.y, sh); w.w = byte_window(hi.y, hi.z, sh);
-      break;
-    default:
-      w.x = byte_window(lo.w, hi.x, sh); w.y = byte_window(hi.x, hi.y, sh);
-      w.z = byte_window(hi.y, hi.z, sh); w.w = byte_window(hi.z, hi.w, sh);
-      break;
-  }
-  return w;
-}
-
-// Same window with the word offset Q = (sel >> 2) & 3 fixed at compile time (callers
-// branch once per warp-uniform step, not once per chunk); sh = 8 * (sel & 3).
+// 16 bytes starting at shared address base16 + sel (base16 16-B aligned, sel in 0..15):
+// two conflict-free LDS.128 + funnel shifts -- SIMDcompare's unaligned load
+// (PAPER.md:101 _mm_loadu_si128) on shared memory.  The word offset Q =
+// (sel >> 2) & 3 is a template parameter (callers branch once per warp-uniform
+// step, not once per chunk); sh = 8 * (sel & 3).
 template <int Q>
 __device__ __forceinline__ uint4 window16_q(const uint8_t* base16, uint32_t sh) {
   const uint4 lo = lds128(base16);
@@ -97,11 +71,6 @@ __device__ __forceinline__ Found4 found_all() { return Found4{0x80808080u, 0x808
 __device__ __forceinline__ Found4 found_from_mask16(uint32_t vmask) {
   return Found4{nibble_to_flags(vmask & 0xFu), nibble_to_flags((vmask >> 4) & 0xFu),
                 nibble_to_flags((vmask >> 8) & 0xFu), nibble_to_flags((vmask >> 12) & 0xFu)};
-}
-
-__device__ __forceinline__ uint32_t found_mask16(const Found4& F) {
-  return flags_to_nibble(F.f0) | (flags_to_nibble(F.f1) << 4) | (flags_to_nibble(F.f2) << 8) |
-         (flags_to_nibble(F.f3) << 12);
 }
 
 __device__ __forceinline__ uint32_t found_any(const Found4& F) { return (F.f0 | F.f1 | F.f2 | F.f3) & 0x80808080u; }

@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""Small workload for compute-sanitizer: every strategy x epilogue, unaligned views,
+"""Edge-case workload for the bounds-checked build (tests/test_gpu_debug_checks.py): every strategy x epilogue, unaligned views,
 ragged ends, batches; checks results against the oracle (test infrastructure)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

@@ -19,7 +19,7 @@ def test_debug_build_bounds_assertions():
     lib = _build.build(debug=True)
     assert os.path.exists(lib)
     env = dict(os.environ, SMGPU_LIB="debug")
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sanitize_run.py")], env=env,
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "debug_workload.py")], env=env,
                        capture_output=True, text=True, timeout=600)
     out = r.stdout + r.stderr
     assert "SMGPU_DCHECK failed" not in out, out[-3000:]
