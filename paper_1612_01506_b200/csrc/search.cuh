@@ -12,10 +12,10 @@ constexpr int kMaxStages = 8;
 constexpr int kGroup = 8;                                // FILTER: chunk-rows per queue fill
 constexpr int kQueueLen = 32 * kGroup;                   // FILTER: queue entries per warp
 constexpr uint32_t kLaneVerifyMaxM = 34;                 // FILTER: per-lane verification up to this m
-constexpr int kMaxBatch = 32;                            // patterns per launch
+constexpr int kMaxBatch = 64;                            // patterns per launch
 constexpr int kListCap = 512;                            // reporting: buffered positions per warp and tile
 constexpr int kTableSmall = 256;                         // pattern-table capacities (u32 entries)
-constexpr int kTableLarge = 7168;                        // fills the 32 KiB kernel-parameter space
+constexpr int kTableLarge = 6400;                        // with 64 descriptors: fills the 32 KiB parameter space
 constexpr int kBatchTableWords = kTableLarge;            // batching: table entries per launch
 
 // shared-memory layout: [full/empty mbarriers][warp totals [2][W]][queue chunk ids u16 [W][kQueueLen]]
