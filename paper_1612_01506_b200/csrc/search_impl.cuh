@@ -115,7 +115,8 @@ struct WorkIter {
   uint64_t next = blockIdx.x;  // next unprobed item
   uint64_t base = 0;           // first item of the current probe
   uint32_t mask = 0;           // non-empty items of the current probe not yet returned
-  __device__ __forceinline__ bool advance(const LaunchParams<CAP>& P, int lane, uint64_t& w) {
+  // k0: pattern of the previously returned item (a lower bound for every later item)
+  __device__ __forceinline__ bool advance(const LaunchParams<CAP>& P, int lane, uint64_t& w, uint32_t k0) {
     const uint64_t total = P.a.total_work, grid = gridDim.x;
     if (EPI != kEpiWrite) {
       if (next >= total) return false;
@@ -129,7 +130,7 @@ struct WorkIter {
       const uint64_t wj = base + (uint64_t)lane * grid;
       bool nonempty = false;
       if (wj < total) {
-        uint32_t kk = 0;
+        uint32_t kk = k0;
         while (wj >= P.d[kk].work_end) ++kk;
         const PatDesc& d = P.d[kk];
         const uint64_t item = d.item_base + wj - (d.work_end - d.ntiles);
@@ -160,7 +161,7 @@ __device__ void produce(const LaunchParams<CAP>& P, uint8_t* ring, uint64_t* ful
   uint32_t k = 0;
   WorkIter<EPI, CAP> items;
   uint64_t w;
-  while (items.advance(P, lane, w)) {
+  while (items.advance(P, lane, w, k)) {
     while (w >= P.d[k].work_end) ++k;
     if (lane != 0) continue;  // lane 0 issues the copies; the warp only probes work items
     const PatDesc& d = P.d[k];
@@ -735,7 +736,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
   uint32_t acc = 0;  // kEpiCount: this lane's matches of pattern k so far
   WorkIter<EPI, CAP> items;
   uint64_t w;
-  while (items.advance(P, lane, w)) {
+  while (items.advance(P, lane, w, k)) {
     while (w >= P.d[k].work_end) {
       if (EPI == kEpiCount) {  // flush pattern k (warp-uniform)
         const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, acc);
