@@ -160,10 +160,12 @@ sm_status sm_report_async(const uint8_t* p, size_t m, const uint8_t* t, size_t n
  * max_alignments, hist, strategy).  d_counts[i] (DEVICE u64[P]) = count of p[i];
  * positions of all patterns are written CONCATENATED in pattern order into DEVICE
  * pos[0..cap): pattern i's ascending positions start at sum_{j<i} d_counts[j].
- * Positions past cap are dropped (the caller detects truncation from d_counts). */
+ * Positions past cap are dropped (the caller detects truncation from d_counts).
+ * position_offset is added to every written position (0 for a whole text; a text
+ * shard passes the global position of its first byte, so its positions are global). */
 sm_status sm_report_batch(const uint8_t* const* p, const size_t* m, size_t P, const uint8_t* t, size_t n,
                           size_t max_alignments, const uint64_t* hist, int strategy, uint64_t* pos, size_t cap,
-                          uint64_t* d_counts, void* stream);
+                          uint64_t* d_counts, uint64_t position_offset, void* stream);
 
 /* Fixed comparison orders of PAPER.md:184-186 (Sec. 2.4), for the order ablation
  * (the paper's N / N-freq / N-fixed columns).  Host-only; order[m] out (0-based).

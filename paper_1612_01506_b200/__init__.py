@@ -83,7 +83,8 @@ def load_library(path: str = LIB_PATH):
     lib.sm_count_batch.restype = ctypes.c_int
     lib.sm_count_batch.argtypes = [_vp, _vp, _sz, _u8p, _sz, _sz, _vp, ctypes.c_int, _vp, _vp]
     lib.sm_report_batch.restype = ctypes.c_int
-    lib.sm_report_batch.argtypes = [_vp, _vp, _sz, _u8p, _sz, _sz, _vp, ctypes.c_int, _vp, _sz, _vp, _vp]
+    lib.sm_report_batch.argtypes = [_vp, _vp, _sz, _u8p, _sz, _sz, _vp, ctypes.c_int, _vp, _sz, _vp,
+                                    ctypes.c_uint64, _vp]
     lib.sm_report_async.restype = ctypes.c_int
     lib.sm_report_async.argtypes = [_u8p, _sz, _u8p, _sz, _vp, _vp, ctypes.c_uint32, ctypes.c_int, _vp, _sz,
                                     _vp, _vp]
@@ -283,7 +284,7 @@ def sm_count_batch(patterns, t, d_counts, hist=None, max_alignments: Optional[in
 
 
 def sm_report_batch(patterns, t, pos, d_counts, hist=None, max_alignments: Optional[int] = None,
-                    strategy: int = SM_STRATEGY_AUTO, stream=None) -> None:
+                    strategy: int = SM_STRATEGY_AUTO, stream=None, position_offset: int = 0) -> None:
     """Enqueue reporting for all patterns: d_counts[P] totals, positions concatenated in pattern
     order into pos (int64 CUDA tensor, capacity pos.numel())."""
     lib = load_library()
@@ -294,7 +295,7 @@ def sm_report_batch(patterns, t, pos, d_counts, hist=None, max_alignments: Optio
     cap = 0 if pos is None else pos.numel()
     pptr = None if pos is None else pos.data_ptr()
     s = lib.sm_report_batch(ctypes.addressof(pb.ptrs), ctypes.addressof(pb.lens), pb.P, tp, n, lim, _np_ptr(h),
-                            strategy, pptr, cap, d_counts.data_ptr(), _stream(stream))
+                            strategy, pptr, cap, d_counts.data_ptr(), int(position_offset), _stream(stream))
     if s != SM_OK:
         _raise(s)
 

@@ -452,7 +452,8 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
 // tiles with matches.  Launches cover consecutive runs of the caller's patterns.
 sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_t P, const uint8_t* t, size_t n,
                                uint64_t lim, const uint64_t* hist, const uint32_t* order, uint32_t peel,
-                               int strategy, uint64_t* pos, size_t cap, uint64_t* d_counts, cudaStream_t st) {
+                               int strategy, uint64_t* pos, size_t cap, uint64_t* d_counts, uint64_t pos_offset,
+                               cudaStream_t st) {
   if (P == 0) return SM_OK;
   SM_CUDA_TRY(cudaMemsetAsync(d_counts, 0, P * sizeof(uint64_t), st), "cudaMemsetAsync(counts)");
   uint64_t hb[256];
@@ -535,6 +536,7 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
       L.a.tile_offsets = offsets;
       L.a.pos = pos;
       L.a.cap = cap;
+      L.a.pos_offset = pos_offset;
       e = launch_search(L, st);
       if (e == cudaSuccess) ++g_launches;
     }
@@ -549,7 +551,7 @@ sm_status enqueue_report(const uint8_t* p, size_t m, const uint8_t* t, size_t n,
                          uint64_t* d_count, cudaStream_t st) {
   const uint8_t* ps[1] = {p};
   const size_t ms[1] = {m};
-  return enqueue_report_batch(ps, ms, 1, t, n, UINT64_MAX, hist, order, peel, strategy, pos, cap, d_count, st);
+  return enqueue_report_batch(ps, ms, 1, t, n, UINT64_MAX, hist, order, peel, strategy, pos, cap, d_count, 0, st);
 }
 
 }  // namespace
@@ -681,7 +683,7 @@ sm_status sm_count_batch(const uint8_t* const* p, const size_t* m, size_t P, con
 
 sm_status sm_report_batch(const uint8_t* const* p, const size_t* m, size_t P, const uint8_t* t, size_t n,
                           size_t max_alignments, const uint64_t* hist, int strategy, uint64_t* pos, size_t cap,
-                          uint64_t* d_counts, void* stream) {
+                          uint64_t* d_counts, uint64_t position_offset, void* stream) {
   if (P == 0) return SM_OK;
   if (!p || !m || !d_counts) return fail(SM_EINVAL, "NULL argument");
   if (strategy < SM_STRATEGY_AUTO || strategy > SM_STRATEGY_PACKED) return fail(SM_EINVAL, "bad strategy");
@@ -703,7 +705,7 @@ sm_status sm_report_batch(const uint8_t* const* p, const size_t* m, size_t P, co
     if (s != SM_OK) return s;
   }
   return enqueue_report_batch(p, m, P, t, n, (uint64_t)max_alignments, hist, nullptr, 0, strategy, pos, cap,
-                              d_counts, as_stream(stream));
+                              d_counts, position_offset, as_stream(stream));
 }
 
 sm_status sm_report_async(const uint8_t* p, size_t m, const uint8_t* t, size_t n, const uint64_t* hist,

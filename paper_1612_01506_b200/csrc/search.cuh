@@ -71,6 +71,7 @@ struct LaunchArgs {
   const uint64_t* tile_offsets;  // kEpiWrite: exclusive prefix of tile_counts (patterns in caller order)
   uint64_t* pos;             // kEpiWrite: output positions
   uint64_t cap;              // kEpiWrite: capacity of pos
+  uint64_t pos_offset;       // kEpiWrite: added to every written position (a shard's first owned position)
 };
 
 // Kernel parameters: everything per launch, no __constant__ state, so launches on

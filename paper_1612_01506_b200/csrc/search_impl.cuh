@@ -666,9 +666,9 @@ __device__ __forceinline__ void write_masks(const LaunchArgs& a, uint32_t* s_wt,
   const uint64_t run = publish_and_offset(a, s_wt, par, warp, lane, w, as.n);
   __syncwarp();
   if (as.n <= (uint32_t)kListCap) {
-    write_list(a, list, as.n, run, x_base - (int64_t)a.delta, lane);
+    write_list(a, list, as.n, run, x_base - (int64_t)a.delta + (int64_t)a.pos_offset, lane);
   } else {
-    WriteSink<IN_G> ws{run, x_base - (int64_t)a.delta, a.pos, a.cap};
+    WriteSink<IN_G> ws{run, x_base - (int64_t)a.delta + (int64_t)a.pos_offset, a.pos, a.cap};
 #pragma unroll
     for (int it = 0; it < CPL; ++it) ws(cw0 + it * 32u + lane, mk[it], lane);
   }
@@ -686,9 +686,9 @@ __device__ __forceinline__ void write_units(const LaunchArgs& a, uint32_t* s_wt,
   const uint64_t run = publish_and_offset(a, s_wt, par, warp, lane, w, as.n);
   __syncwarp();
   if (as.n <= (uint32_t)kListCap) {
-    write_list(a, list, as.n, run, x_base - (int64_t)a.delta, lane);
+    write_list(a, list, as.n, run, x_base - (int64_t)a.delta + (int64_t)a.pos_offset, lane);
   } else {
-    WriteSink<false> ws{run, x_base - (int64_t)a.delta, a.pos, a.cap};
+    WriteSink<false> ws{run, x_base - (int64_t)a.delta + (int64_t)a.pos_offset, a.pos, a.cap};
 #pragma unroll
     for (int it = 0; it < CPL; ++it)
       if (it < units) ws.add(mbase[it], mk[it], lane);
@@ -778,9 +778,9 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
         filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, as);
         uint64_t run = publish_and_offset(a, s_wt, par, warp, lane, d.item_base + ti, as.n);
         if (as.n <= (uint32_t)kListCap) {
-          write_list(a, list, as.n, run, x_base - (int64_t)a.delta, lane);
+          write_list(a, list, as.n, run, x_base - (int64_t)a.delta + (int64_t)a.pos_offset, lane);
         } else {  // list overflow (very dense tile): ranked writes from a recomputation
-          WriteSink<> ws{run, x_base - (int64_t)a.delta, a.pos, a.cap};
+          WriteSink<> ws{run, x_base - (int64_t)a.delta + (int64_t)a.pos_offset, a.pos, a.cap};
           filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, ws);
         }
         par ^= 1u;

@@ -103,3 +103,54 @@ def count_sharded(patterns, shard_text, shard: Shard, hist, counts=None, group=N
     sm.sm_count_batch(pb, held, counts, hist=hist, max_alignments=shard.owned_bytes, strategy=strategy,
                       stream=stream)
     return allreduce_sum_(counts, group)
+
+
+def gather_reports(local_counts, local_pos, group=None):
+    """Combine per-rank reports (NEXT-4): every rank passes its int64[P] counts and its
+    positions concatenated by pattern (global positions, ascending within a pattern).
+    Returns (global counts int64[P], global positions concatenated by pattern) on every
+    rank.  Ranks own ascending contiguous alignment ranges, so pattern k's global list
+    is rank 0's segment k, then rank 1's, ... (already sorted)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return local_counts, local_pos
+    world = dist.get_world_size(group)
+    P = local_counts.numel()
+    counts = [torch.empty_like(local_counts) for _ in range(world)]
+    dist.all_gather(counts, local_counts, group=group)
+    totals = [int(c.sum().item()) for c in counts]
+    width = max(max(totals), 1)
+    padded = torch.zeros(width, dtype=local_pos.dtype, device=local_pos.device)
+    padded[: local_pos.numel()] = local_pos
+    gathered = [torch.empty_like(padded) for _ in range(world)]
+    dist.all_gather(gathered, padded, group=group)
+    starts = [torch.cumsum(c, 0) - c for c in counts]  # segment start of pattern k on rank r
+    cnt = [c.tolist() for c in counts]
+    st = [s.tolist() for s in starts]
+    pieces = []
+    for k in range(P):
+        for r in range(world):
+            if cnt[r][k]:
+                pieces.append(gathered[r][st[r][k]: st[r][k] + cnt[r][k]])
+    pos = torch.cat(pieces) if pieces else local_pos[:0]
+    return torch.stack(counts).sum(0), pos
+
+
+def report_sharded(patterns, shard_text, shard: Shard, hist, group=None, stream=None, strategy: int = 0):
+    """Global reports: each rank reports the occurrences at its owned alignments as global
+    positions (position_offset = its first owned position), then gather_reports."""
+    import torch
+
+    import paper_1612_01506_b200 as sm
+    pb = patterns if isinstance(patterns, sm.PatternBatch) else sm.PatternBatch(patterns)
+    shard.view_len(max((len(p) for p in pb.data), default=1))  # halo check
+    held = shard_text[: shard.held_len]
+    counts = torch.zeros(max(pb.P, 1), dtype=torch.int64, device=shard_text.device)[: pb.P]
+    sm.sm_report_batch(pb, held, None, counts, hist=hist, max_alignments=shard.owned_bytes, strategy=strategy,
+                       stream=stream)  # sizing call (cap 0: counts only)
+    total = int(counts.sum().item())
+    pos = torch.empty(max(total, 1), dtype=torch.int64, device=shard_text.device)[:total]
+    sm.sm_report_batch(pb, held, pos if total else None, counts, hist=hist, max_alignments=shard.owned_bytes,
+                       strategy=strategy, stream=stream, position_offset=shard.own_lo)
+    return gather_reports(counts, pos, group)

@@ -70,6 +70,49 @@ def test_sharded_counts_and_hist_allreduce(world):
     assert counts == [oracle.naive_count(p, text) for p in pats]
 
 
+def _report_worker(rank, world, port, text, patterns, halo, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sh = smd.make_shard(len(text), rank, world, halo)
+        held = text[sh.own_lo: sh.held_hi]
+        counts, pos = [], []
+        for p in patterns:  # this rank's owned occurrences, as global positions
+            r = oracle.naive_report(p, held[: sh.view_len(len(p))]).astype(np.int64) + sh.own_lo
+            counts.append(r.size)
+            pos.append(r)
+        c = torch.tensor(counts, dtype=torch.int64)
+        ps = torch.from_numpy(np.concatenate(pos)) if pos else torch.zeros(0, dtype=torch.int64)
+        gc, gp = smd.gather_reports(c, ps)
+        q.put((rank, gc.tolist(), gp.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_report_gather(world):
+    rng = np.random.default_rng(50 + world)
+    n = 9001
+    text = rng.integers(0, 2, n, dtype=np.uint8)
+    cuts = smd.shard_bounds(n, world)[1:-1]
+    pats = [text[c - 2: c + 3].tobytes() for c in cuts] + [b"\x01", b"\x00\x00", text[100:108].tobytes()]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_report_worker, args=(r, world, port, text, pats, 15, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want_c = [oracle.naive_count(p, text) for p in pats]
+    want_p = np.concatenate([oracle.naive_report(p, text) for p in pats]).astype(np.int64).tolist()
+    for rank, gc, gp in res:
+        assert gc == want_c and gp == want_p, rank
+
+
 def test_shard_bounds_and_views():
     for N in (0, 1, 15, 16, 17, 1000, 2 ** 20 + 3):
         for G in (1, 2, 3, 8):

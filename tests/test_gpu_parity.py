@@ -446,3 +446,30 @@ def test_concurrent_streams(sm):
     torch.cuda.synchronize()
     for a, pats, d in jobs:
         assert d.cpu().tolist() == [oracle.naive_count(p, a) for p in pats]
+
+
+def test_report_sharded_virtual(sm):
+    """NEXT-4: per-shard reports with global positions (position_offset), concatenated per
+    pattern in rank order == the 1-GPU report."""
+    from paper_1612_01506_b200 import dist
+    rng = np.random.default_rng(64)
+    a = rng.integers(0, 3, (1 << 20) + 123, dtype=np.uint8)
+    t = dev(a)
+    N = a.size
+    h = oracle.hist(a)
+    pats = [a[c - 3: c + 4].tobytes() for c in dist.shard_bounds(N, 8)[1:-1]] + [b"\x01\x02", a[:9].tobytes()]
+    want_c = [oracle.naive_count(p, a) for p in pats]
+    want = [oracle.naive_report(p, a).astype(np.int64) for p in pats]
+    for G in (1, 2, 3, 8):
+        per_rank = []
+        for sh in dist.all_shards(N, G, halo=63):
+            c, p = dist.report_sharded(pats, t[sh.own_lo: sh.held_hi], sh, hist=h)
+            per_rank.append((c.cpu().numpy(), p.cpu().numpy()))
+        tot = sum(c for c, _ in per_rank)
+        assert tot.tolist() == want_c, G
+        for k in range(len(pats)):
+            segs = []
+            for c, p in per_rank:
+                s0 = int(c[:k].sum())
+                segs.append(p[s0: s0 + int(c[k])])
+            assert np.concatenate(segs).tolist() == want[k].tolist(), (G, k)
