@@ -184,6 +184,22 @@ sm_status sm_heuristic_order(const uint8_t* p, size_t m, int kind, uint8_t space
 sm_status sm_plan(const uint8_t* p, size_t m, const uint64_t* hist, const uint32_t* order,
                   uint32_t peel, int strategy, int* strategy_out, uint32_t* peel_out);
 
+/* Compare-step counters (NEXT-2 instrumentation; PAPER.md:34,176-178 discuss how many
+ * comparisons the method executes).  Only the instrumented build libsmgpu_counters.so
+ * (compiled with -DSMGPU_COUNTERS) counts; the release library returns SM_EINVAL.
+ * Synchronises the device, copies the device-wide totals since the last reset into
+ * out[0..8) (host) and, if reset != 0, zeroes them:
+ *   out[0] (warp, work item) pairs processed
+ *   out[1] BLOCK/PACKED warp-blocks (512 x CPL consecutive alignments) holding >= 1
+ *          valid alignment -- Alg. 4's blocks at alpha = out[7]
+ *   out[2] BLOCK/PACKED SIMDcompare steps executed in those blocks (peeled + loop)
+ *   out[3] FILTER 16-alignment chunks whose pi(1)-bytes were tested
+ *   out[4] FILTER chunks holding p[pi(1)]
+ *   out[5] FILTER valid alignments matching pi(1) and pi(2)
+ *   out[6] FILTER pattern positions compared while verifying those
+ *   out[7] BLOCK/PACKED alignments per warp-block (max over launches) */
+sm_status sm_counters(uint64_t* out, int reset);
+
 /* Thread-local status of the last failing call on this thread (SM_OK if none
  * since sm_clear_error), its message, and a static name for a status. */
 sm_status sm_last_error(void);

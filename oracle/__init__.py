@@ -62,6 +62,9 @@ def _load():
         lib.oracle_alg4_count.restype = ctypes.c_uint64
         lib.oracle_alg4_count.argtypes = [_u8p, ctypes.c_size_t, _u8p, ctypes.c_size_t, ctypes.c_uint,
                                           _u32p, ctypes.c_uint, _u64p, _u64p, ctypes.c_uint64]
+        lib.oracle_alg4_steps.restype = ctypes.c_uint64
+        lib.oracle_alg4_steps.argtypes = [_u8p, ctypes.c_size_t, _u8p, ctypes.c_size_t, ctypes.c_size_t,
+                                          _u32p, ctypes.c_uint, _u64p]
         lib.oracle_pi_h.restype = None
         lib.oracle_pi_h.argtypes = [ctypes.c_size_t, _u32p]
         lib.oracle_kmp_count.restype = ctypes.c_uint64
@@ -146,6 +149,23 @@ def alg4_count(p, t, alpha: int = 32, pi: Sequence[int] | None = None, r: int = 
     c = int(lib.oracle_alg4_count(_ptr(pa), m, _ptr(ta), ta.size, alpha, _ptr(pia, _u32p), r,
                                   ctypes.byref(ncmp), None, 0))
     return c, int(ncmp.value)
+
+
+def alg4_steps(p, t, alpha: int, pi: Sequence[int] | None = None, r: int = 1):
+    """SIMDcompare calls and alpha-blocks of Alg. 4 for any alpha >= 1.
+
+    Instrumentation for the NEXT-2 compare counters.  Returns (n_compares, n_blocks)."""
+    pa, ta = _u8(p), _u8(t)
+    m = pa.size
+    if pi is None:
+        pi = np.arange(m, dtype=np.uint32)
+    pia = np.ascontiguousarray(np.asarray(pi, dtype=np.uint32))
+    if m == 0:
+        pia = np.zeros(1, dtype=np.uint32)
+    nb = ctypes.c_uint64(0)
+    c = int(_load().oracle_alg4_steps(_ptr(pa), m, _ptr(ta), ta.size, alpha, _ptr(pia, _u32p), r,
+                                      ctypes.byref(nb)))
+    return c, int(nb.value)
 
 
 def pi_h(m: int) -> np.ndarray:

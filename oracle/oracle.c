@@ -179,6 +179,49 @@ uint64_t oracle_alg4_count(const uint8_t *p, size_t m, const uint8_t *t, size_t 
 }
 
 /* ------------------------------------------------------------------------ */
+/* Alg. 4 for any block width alpha >= 1, instrumentation  */
+/* only (NEXT-2 compare counters): the number of SIMDcompare calls executed   */
+/* and the number of alpha-blocks visited.  Same loop as oracle_alg4_count --  */
+/* blocks i = 1, 1+alpha, ... <= n-m+1 (line 3); r peeled compares without a  */
+/* test; then the pi-ordered loop leaving the block as soon as */
+/* found is empty (lines 8-11) -- with `found` held as one flag per alignment  */
+/* instead of a machine word, so alpha is not limited to 64 (the GPU's warp   */
+/* covers 512 x CPL alignments).  Readings R7 (alignments past n-m+1 masked),  */
+/* R9 (r <- min(r, m)).  Returns the SIMDcompare count; *n_blocks receives    */
+/* the number of blocks.                                                       */
+/* ------------------------------------------------------------------------ */
+uint64_t oracle_alg4_steps(const uint8_t *p, size_t m, const uint8_t *t, size_t n,
+                           size_t alpha, const uint32_t *pi, unsigned r, uint64_t *n_blocks)
+{
+    const uint8_t *P = p - 1, *T = t - 1;
+    uint64_t compares = 0, blocks = 0;
+    if (n_blocks) *n_blocks = 0;
+    if (m == 0 || n < m || alpha == 0) return 0;
+    if (r < 1) r = 1;
+    if (r > m) r = (unsigned)m;                                   /* R9 */
+    unsigned char *found = (unsigned char *)malloc(alpha);
+    if (!found) return 0;
+    size_t last = n - m + 1;
+    for (size_t i = 1; i <= last; i += alpha) {                   /* line 3 */
+        blocks++;
+        size_t width = (last - i + 1 < alpha) ? last - i + 1 : alpha;   /* R7 */
+        for (size_t k = 0; k < width; k++) found[k] = 1;         /* "11..1" */
+        size_t alive = width;
+        size_t j;
+        for (j = 1; j <= m; j++) {
+            if (j > r && alive == 0) break;                       /* lines 6-7 / 10-11 */
+            size_t pj = (size_t)pi[j - 1] + 1;                    /* pi(j), 1-based */
+            for (size_t k = 0; k < width; k++)                    /* SIMDcompare, bit k */
+                if (found[k] && T[i + k + pj - 1] != P[pj]) { found[k] = 0; alive--; }
+            compares++;
+        }
+    }
+    free(found);
+    if (n_blocks) *n_blocks = blocks;
+    return compares;
+}
+
+/* ------------------------------------------------------------------------ */
 /* Fixed heuristic order pi_h (Sec. 2.4):                      */
 /*   p[1], p[m], p[4], p[7], ..., p[3], p[6], ..., p[2], p[5], ...           */
 /* Reading R18: stride-3 chains starting at 4, then 3, then 2, skipping       */

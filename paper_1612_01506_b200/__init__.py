@@ -28,8 +28,10 @@ from typing import Optional, Sequence, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# SMGPU_LIB=debug selects the bounds-checked build (libsmgpu_debug.so, tests only)
-LIB_PATH = os.path.join(_HERE, "libsmgpu_debug.so" if os.environ.get("SMGPU_LIB") == "debug" else "libsmgpu.so")
+# SMGPU_LIB=debug selects the bounds-checked build (libsmgpu_debug.so, tests only);
+# SMGPU_LIB=counters the compare-step instrumented build (libsmgpu_counters.so, NEXT-2)
+_VARIANTS = {"debug": "libsmgpu_debug.so", "counters": "libsmgpu_counters.so"}
+LIB_PATH = os.path.join(_HERE, _VARIANTS.get(os.environ.get("SMGPU_LIB", ""), "libsmgpu.so"))
 
 SM_OK, SM_EINVAL, SM_ETRUNC, SM_ENOMEM, SM_ECUDA = 0, 1, 2, 3, 4
 SM_STRATEGY_AUTO, SM_STRATEGY_FILTER, SM_STRATEGY_BLOCK, SM_STRATEGY_PACKED = 0, 1, 2, 3
@@ -40,8 +42,10 @@ STRATEGY_NAMES = {1: "filter", 2: "block", 3: "packed1", 4: "packed2"}
 EXPORTED_SYMBOLS = (
     "sm_count", "sm_report", "sm_symbol_order", "sm_histogram", "sm_order_from_histogram",
     "sm_count_async", "sm_count_batch", "sm_report_async", "sm_report_batch", "sm_heuristic_order", "sm_plan", "sm_last_error", "sm_last_error_message",
-    "sm_clear_error", "sm_status_string", "sm_version", "sm_launch_count",
+    "sm_clear_error", "sm_status_string", "sm_version", "sm_launch_count", "sm_counters",
 )
+COUNTER_NAMES = ("warp_tiles", "blocks", "steps", "filter_chunks", "filter_queued", "filter_survivors",
+                 "filter_verify", "alpha_eff")
 
 
 class SmError(RuntimeError):
@@ -105,6 +109,8 @@ def load_library(path: str = LIB_PATH):
     lib.sm_version.argtypes = []
     lib.sm_launch_count.restype = ctypes.c_uint64
     lib.sm_launch_count.argtypes = []
+    lib.sm_counters.restype = ctypes.c_int
+    lib.sm_counters.argtypes = [_vp, ctypes.c_int]
     _lib = lib
     return lib
 
@@ -348,6 +354,13 @@ def sm_last_error() -> Tuple[int, str]:
 
 def sm_launch_count() -> int:
     return int(load_library().sm_launch_count())
+
+
+def sm_counters(reset: bool = False) -> dict:
+    """Compare-step counters of the instrumented build (SMGPU_LIB=counters), see smgpu.h."""
+    out = np.zeros(8, dtype=np.uint64)
+    _raise(load_library().sm_counters(out.ctypes.data, int(reset)))
+    return {k: int(v) for k, v in zip(COUNTER_NAMES, out)}
 
 
 def sm_version() -> str:

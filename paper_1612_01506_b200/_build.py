@@ -12,6 +12,7 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libsmgpu.so")
 LIB_DEBUG = os.path.join(HERE, "libsmgpu_debug.so")
+LIB_COUNTERS = os.path.join(HERE, "libsmgpu_counters.so")
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",
@@ -34,18 +35,20 @@ def _stale(lib: str = LIB) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
-    """debug=True: libsmgpu_debug.so with device-side bounds assertions (-DSMGPU_DEBUG_CHECKS)."""
-    lib = LIB_DEBUG if debug else LIB
+def build(force: bool = False, verbose: bool = False, debug: bool = False, counters: bool = False) -> str:
+    """debug=True: libsmgpu_debug.so with device-side bounds assertions (-DSMGPU_DEBUG_CHECKS);
+    counters=True: libsmgpu_counters.so with compare-step counters (-DSMGPU_COUNTERS)."""
+    lib = LIB_DEBUG if debug else (LIB_COUNTERS if counters else LIB)
     if not force and not _stale(lib):
         return lib
-    objdir = os.path.join(HERE, "build_debug" if debug else "build")
+    objdir = os.path.join(HERE, "build_debug" if debug else ("build_counters" if counters else "build"))
+    defs = (["-DSMGPU_DEBUG_CHECKS"] if debug else []) + (["-DSMGPU_COUNTERS"] if counters else [])
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = ["nvcc", *NVCC_FLAGS, *(["-DSMGPU_DEBUG_CHECKS"] if debug else []), "-I", INCLUDE, "-I", CSRC,
+        cmd = ["nvcc", *NVCC_FLAGS, *defs, "-I", INCLUDE, "-I", CSRC,
                "-c", src, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
@@ -67,4 +70,5 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False) -> st
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, debug="--debug" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, debug="--debug" in sys.argv,
+                counters="--counters" in sys.argv))

@@ -37,6 +37,24 @@ sm_status cuda_fail(cudaError_t e, const char* what) {
     if (_e != cudaSuccess) return cuda_fail(_e, what); \
   } while (0)
 
+#ifdef SMGPU_COUNTERS
+// instrumented build: one device u64[kCounters] per device, accumulated by every launch
+unsigned long long* counters_ptr() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  static unsigned long long* bufs[64] = {nullptr};
+  if (!bufs[dev]) {
+    void* q = nullptr;
+    if (cudaMalloc(&q, kCounters * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+    cudaMemset(q, 0, kCounters * sizeof(unsigned long long));
+    bufs[dev] = static_cast<unsigned long long*>(q);
+  }
+  return bufs[dev];
+}
+#else
+unsigned long long* counters_ptr() { return nullptr; }
+#endif
+
 int num_sms() {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 148;
@@ -316,6 +334,7 @@ void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_
     }
   L.a.npat = (uint32_t)ps.size();
   L.a.tbl_words = (uint32_t)L.e.size();
+  L.a.ctr = counters_ptr();
   // reporting launches reserve the per-warp position lists
   L.a.list_off = (kTblOff + 127) & ~127u;
   const uint32_t list_bytes = epilogue == kEpiCount ? 0u : (uint32_t)(kConsumerWarps * kListCap * 2);
@@ -445,11 +464,46 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
   return SM_OK;
 }
 
+// Staging pool of the reporting pass (bytes): enough for ~4 bytes per reported
+// position plus 64 MiB, at most 2 GiB; SMGPU_STAGE_BYTES overrides (tests force the
+// overflow path with a tiny pool).  Tiles whose record does not fit are recomputed
+// from the text by the overflow pass, so the size never changes results.
+uint64_t stage_pool_bytes(uint64_t cap) {
+  static const long long env = [] {
+    const char* e = std::getenv("SMGPU_STAGE_BYTES");
+    return e ? std::atoll(e) : -1LL;
+  }();
+  uint64_t b = env >= 0 ? (uint64_t)env : std::min<uint64_t>(2ull << 30, (64ull << 20) + 4 * cap);
+  return (b + 15) & ~15ull;
+}
+
+// The stream-ordered allocator returns freed blocks to the driver at every
+// synchronisation by default; keep them cached so per-call report scratch costs no
+// remapping (once per device).
+void keep_pool_cached() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  static bool done[64] = {false};
+  if (done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
 // Reporting (A8) for P patterns, output concatenated in pattern order: pattern k's
 // ascending positions at pos[off_k ..), off_k = sum of earlier counts (first `cap`
-// positions overall are written).  Pass 1: per-(pattern, tile) counts and per-pattern
-// totals; one exclusive scan over all work items; pass 2 writes, visiting only
-// tiles with matches.  Launches cover consecutive runs of the caller's patterns.
+// positions overall are written).  One read of the text per pattern:
+//   pass 1 (kEpiStage): per-(item, warp) counts + per-pattern totals, and each warp's
+//          matches in an item staged as a compact record (u16 list / bitmap) in the
+//          warp's own chunk of the staging pool;
+//   one exclusive scan over all work items (pattern-major in caller order);
+//   expand: records -> positions at the scanned offsets;
+//   overflow pass (kEpiWrite): tiles whose record did not fit the pool, recomputed
+//          from the text (no work at all when the pool sufficed).
+// cap == 0 (the two-call idiom's first call): counts only.
 sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_t P, const uint8_t* t, size_t n,
                                uint64_t lim, const uint64_t* hist, const uint32_t* order, uint32_t peel,
                                int strategy, uint64_t* pos, size_t cap, uint64_t* d_counts, uint64_t pos_offset,
@@ -473,6 +527,7 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
     plans.push_back(std::move(q));
   }
   if (plans.empty()) return SM_OK;
+  const int epi1 = cap > 0 ? kEpiStage : kEpiCount;
   // launches grouped by strategy (batch limits as for counting); every pattern keeps
   // a fixed slot range [item_base, item_base + ntiles) of the per-tile arrays in the
   // caller's order, so one scan gives the concatenated, pattern-ordered output layout
@@ -483,7 +538,7 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
     auto flush = [&]() {
       if (run.empty()) return;
       Ls.emplace_back();
-      build_launch(run, t, n, lim, kEpiTileCount, Ls.back());
+      build_launch(run, t, n, lim, epi1, Ls.back());
       run.clear();
       words = 0;
     };
@@ -495,51 +550,78 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
     }
     flush();
   }
+  if (cap == 0) {  // totals only
+    for (HostLaunch& L : Ls) {
+      sm_status s = launch_checked(L, st, "search kernel (report totals)");
+      if (s != SM_OK) return s;
+    }
+    return SM_OK;
+  }
   // item bases in pattern order (a descriptor's pattern index = its count_out - d_counts)
   std::vector<PatDesc*> slot(P, nullptr);
   for (HostLaunch& L : Ls)
     for (PatDesc& d : L.d) slot[(size_t)(d.count_out - d_counts)] = &d;
-  uint64_t item = 0;
+  uint64_t items = 0;
   for (size_t i = 0; i < P; ++i)
     if (slot[i]) {
-      slot[i]->item_base = item;
-      item += slot[i]->ntiles;
+      slot[i]->item_base = items;
+      items += slot[i]->ntiles;
     }
-  uint64_t total_work = 0;
-  for (const HostLaunch& L : Ls) total_work += L.a.total_work;
-  const uint64_t nt1 = total_work + 1;
+  if (items >= (1ull << 32)) return fail(SM_EINVAL, "report: more than 2^32 (pattern, tile) work items in one call");
+  keep_pool_cached();
   size_t temp_bytes = 0;
-  SM_CUDA_TRY(exclusive_scan_u64(nullptr, nullptr, nt1, nullptr, &temp_bytes, st), "scan sizing");
-  const size_t off_bytes = ((nt1 * 8 + 255) / 256) * 256;
+  SM_CUDA_TRY(exclusive_scan_wc(nullptr, nullptr, items, nullptr, &temp_bytes, st), "scan sizing");
+  auto al = [](uint64_t b) { return (b + 255) & ~255ull; };
+  const uint64_t nL = Ls.size();
+  const uint64_t wc_b = al(items * 16), offs_b = al(items * 8), bits_b = al((items + 31) / 32 * 4),
+                 ovf_b = al(items * 4), ctr_b = al(8 + nL * 4), temp_b = al(temp_bytes),
+                 stage_b = stage_pool_bytes(cap);
   uint8_t* scratch = nullptr;
-  SM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&scratch), 2 * off_bytes + temp_bytes, st),
+  SM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+                              wc_b + bits_b + ctr_b + offs_b + ovf_b + temp_b + stage_b, st),
               "cudaMallocAsync(report scratch)");
-  uint64_t* counts = reinterpret_cast<uint64_t*>(scratch);
-  uint64_t* offsets = reinterpret_cast<uint64_t*>(scratch + off_bytes);
-  void* temp = scratch + 2 * off_bytes;
-  cudaError_t e = cudaMemsetAsync(counts, 0, nt1 * 8, st);
-  for (HostLaunch& L : Ls) {  // pass 1
+  uint8_t* q = scratch;  // zero-initialised part first: wc, ovf_bits, counters
+  uint16_t* wc = reinterpret_cast<uint16_t*>(q); q += wc_b;
+  uint32_t* ovf_bits = reinterpret_cast<uint32_t*>(q); q += bits_b;
+  unsigned long long* stage_used = reinterpret_cast<unsigned long long*>(q);
+  uint32_t* ovf_n = reinterpret_cast<uint32_t*>(q + 8); q += ctr_b;
+  uint64_t* offsets = reinterpret_cast<uint64_t*>(q); q += offs_b;
+  uint32_t* ovf_items = reinterpret_cast<uint32_t*>(q); q += ovf_b;
+  void* temp = q; q += temp_b;
+  uint8_t* stage = q;
+  cudaError_t e = cudaMemsetAsync(scratch, 0, wc_b + bits_b + ctr_b, st);
+  uint64_t ovf_at = 0;
+  for (size_t li = 0; li < Ls.size(); ++li) {  // pass 1: per-warp counts + staged records
     if (e != cudaSuccess) break;
-    L.a.tile_counts = counts;
+    HostLaunch& L = Ls[li];
+    L.a.wc = wc;
+    L.a.stage = stage;
+    L.a.stage_used = stage_used;
+    L.a.stage_cap16 = stage_b / 16;
+    L.a.ovf_bits = ovf_bits;
+    L.a.ovf_items = ovf_items + ovf_at;  // this launch's overflow queue (capacity: its items)
+    L.a.ovf_n = ovf_n + li;
+    L.a.pos_offset = pos_offset;
+    ovf_at += L.a.total_work;
     e = launch_search(L, st);
     if (e == cudaSuccess) ++g_launches;
   }
   if (e == cudaSuccess) {
-    e = exclusive_scan_u64(counts, offsets, nt1, temp, &temp_bytes, st);
+    e = exclusive_scan_wc(wc, offsets, items, temp, &temp_bytes, st);
     if (e == cudaSuccess) g_launches += 1;
   }
-  if (cap > 0) {
-    for (HostLaunch& L : Ls) {  // pass 2
-      if (e != cudaSuccess) break;
-      L.epilogue = kEpiWrite;
-      L.a.tile_counts = nullptr;
-      L.a.tile_offsets = offsets;
-      L.a.pos = pos;
-      L.a.cap = cap;
-      L.a.pos_offset = pos_offset;
-      e = launch_search(L, st);
-      if (e == cudaSuccess) ++g_launches;
-    }
+  if (e == cudaSuccess) {
+    e = launch_stage_expand(stage, stage_used, stage_b / 16, wc, offsets, pos, cap, num_sms(), st);
+    if (e == cudaSuccess) ++g_launches;
+  }
+  for (HostLaunch& L : Ls) {  // overflow pass (CTAs exit at once when the queue is empty)
+    if (e != cudaSuccess) break;
+    L.epilogue = kEpiWrite;
+    L.a.tile_offsets = offsets;
+    L.a.pos = pos;
+    L.a.cap = cap;
+    e = launch_search(L, st);
+    if (e == cudaSuccess) ++g_launches;
   }
   cudaFreeAsync(scratch, st);
   if (e != cudaSuccess) return cuda_fail(e, "report");
@@ -789,7 +871,23 @@ const char* sm_status_string(sm_status s) {
   return "SM_UNKNOWN";
 }
 
-const char* sm_version(void) { return "smgpu 0.1 (sm_100a)"; }
+sm_status sm_counters(uint64_t* out, int reset) {
+  if (!out) return fail(SM_EINVAL, "out is NULL");
+  unsigned long long* d = counters_ptr();
+  if (!d) return fail(SM_EINVAL, "not the instrumented build (libsmgpu_counters.so, -DSMGPU_COUNTERS)");
+  SM_CUDA_TRY(cudaDeviceSynchronize(), "sm_counters sync");
+  SM_CUDA_TRY(cudaMemcpy(out, d, kCounters * sizeof(uint64_t), cudaMemcpyDeviceToHost), "sm_counters copy");
+  if (reset) SM_CUDA_TRY(cudaMemset(d, 0, kCounters * sizeof(uint64_t)), "sm_counters reset");
+  return SM_OK;
+}
+
+const char* sm_version(void) {
+#ifdef SMGPU_COUNTERS
+  return "smgpu 0.1 (sm_100a, compare counters)";
+#else
+  return "smgpu 0.1 (sm_100a)";
+#endif
+}
 uint64_t sm_launch_count(void) { return g_launches; }
 
 }  // extern "C"

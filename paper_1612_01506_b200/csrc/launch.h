@@ -26,6 +26,17 @@ cudaError_t launch_hist(const uint8_t* t, uint64_t n, uint64_t* d_hist, int num_
 
 cudaError_t launch_search(const HostLaunch& L, cudaStream_t stream);
 
+// Reporting: expand the staged records of the pool (chunks [0, min(*stage_used,
+// stage_cap16)) into positions pos[tile_offsets[item] + warps before + j] (< cap),
+// see search.cuh.
+cudaError_t launch_stage_expand(const uint8_t* stage, const unsigned long long* stage_used, uint64_t stage_cap16,
+                                const uint16_t* wc, const uint64_t* tile_offsets, uint64_t* pos, uint64_t cap,
+                                int num_sms, cudaStream_t st);
+
+// exclusive prefix over items of the sum of wc[item][0..8) (u16 warp counts)
+cudaError_t exclusive_scan_wc(const uint16_t* wc, uint64_t* out, uint64_t items, void* temp, size_t* temp_bytes,
+                              cudaStream_t st);
+
 cudaError_t exclusive_scan_u64(const uint64_t* in, uint64_t* out, uint64_t count, void* temp, size_t* temp_bytes,
                                cudaStream_t st);
 

@@ -13,7 +13,7 @@ constexpr int kGroup = 8;                                // FILTER: chunk-rows p
 constexpr int kQueueLen = 32 * kGroup;                   // FILTER: queue entries per warp
 constexpr uint32_t kLaneVerifyMaxM = 34;                 // FILTER: per-lane verification up to this m
 constexpr int kMaxBatch = 64;                            // patterns per launch
-constexpr int kListCap = 512;                            // reporting: buffered positions per warp and tile
+constexpr int kListCap = 512;                            // reporting (overflow pass): buffered positions per warp and tile
 constexpr int kTableSmall = 256;                         // pattern-table capacities (u32 entries)
 constexpr int kTableLarge = 6400;                        // with 64 descriptors: fills the 32 KiB parameter space
 constexpr int kBatchTableWords = kTableLarge;            // batching: table entries per launch
@@ -25,7 +25,30 @@ constexpr uint32_t kQueueOff = kWarpTotOff + 2 * kConsumerWarps * 4;
 constexpr uint32_t kTblOff = kQueueOff + kConsumerWarps * kQueueLen * 2;  // end of the fixed region
 
 enum Strategy : int { kFilter = 1, kBlock = 2, kPacked1 = 3, kPacked2 = 4 };  // kPackedB: b-bit codes
-enum Epilogue : int { kEpiCount = 0, kEpiTileCount = 1, kEpiWrite = 2 };
+// kEpiCount: per-pattern counts.  kEpiStage: reporting pass 1 -- per-(pattern, tile) counts
+// plus the tile's matches staged compactly in global memory (per-warp u16 offset lists
+// or bitmaps), expanded into positions by stage_expand_kernel after the scan: the
+// text is read once.  kEpiWrite: reporting fallback for the tiles whose staging did
+// not fit the pool (overflow queue): recompute from the text, write positions.
+enum Epilogue : int { kEpiCount = 0, kEpiStage = 1, kEpiWrite = 2 };
+
+// Staged reporting (kEpiStage): every compare warp with matches in a work item writes
+// one self-describing record into its own chunk of the staging pool (kStageChunk
+// 16-B units per chunk, grabbed with one global atomic; records packed back to back,
+// a zero header terminates a chunk's records):
+//   header (16 B): i64 pos_base (0-based position of tile-relative alignment u = 0,
+//                  shard offset included), u32 item, u16 cnt, u8 warp, u8 log2(CPL);
+//   data: when 2 cnt < wspan / 8 (wspan = 512 CPL alignments per warp) the ascending
+//         u16 list of the tile-relative alignments u (padded to 16 B), else the warp's
+//         bitmap, wspan / 16 u16 words, bit b of word i <-> u = warp wspan + 16 i + b.
+// and posts cnt into wc[item][warp] (u16 x 8 per item, zero-initialised): the scan of
+// the per-item sums gives each item's output offset, wc its warps' order inside it.
+constexpr uint32_t kRecHeader = 16;
+constexpr uint32_t kStageChunk = 1024;  // 16-B units (16 KiB) >= largest record + terminator
+__host__ __device__ inline uint32_t rec_warp_bytes(uint32_t cnt, uint32_t wspan) {
+  if (cnt == 0) return 0;
+  return 2u * cnt < wspan / 8u ? ((2u * cnt + 15u) & ~15u) : wspan / 8u;
+}
 
 // One pattern of a launch.  Byte offsets are relative to `base` = align_down(t, 16);
 // the text occupies offsets [delta, delta + n); alignment offset x <-> position x - delta.
@@ -38,8 +61,8 @@ struct PatDesc {
   uint64_t work_end;   // this pattern's work items are [work_end - ntiles, work_end)
   uint64_t edge_lo;    // tiles ti < edge_lo start before the first alignment
   uint64_t edge_hi;    // tiles ti >= edge_hi end after the last alignment
-  uint64_t* count_out; // kEpiCount / kEpiTileCount: device u64 (accumulated with atomics; zeroed by host)
-  uint64_t item_base;  // reporting: index of this pattern's first tile in tile_counts / tile_offsets
+  uint64_t* count_out; // kEpiCount / kEpiStage: device u64 (accumulated with atomics; zeroed by host)
+  uint64_t item_base;  // reporting: index of this pattern's first tile in wc / tile_offsets
   uint32_t m;
   uint32_t r;          // peeling factor (BLOCK), 1 <= r <= m
   uint32_t a1;         // pattern offset of pi(1) (FILTER)
@@ -67,11 +90,31 @@ struct LaunchArgs {
   uint32_t pack_off;         // PACKED: smem byte offset of the double-buffered code array
   uint32_t pack_bytes;       // PACKED: bytes of one code buffer
   uint32_t list_off;         // reporting: smem byte offset of the per-warp position lists [W][kListCap] u16
-  uint64_t* tile_counts;     // kEpiTileCount: u64 per (pattern, tile), at item_base + ti (zeroed by host)
-  const uint64_t* tile_offsets;  // kEpiWrite: exclusive prefix of tile_counts (patterns in caller order)
+  uint16_t* wc;              // kEpiStage: per item u16[kConsumerWarps] match counts (zeroed by host)
+  uint8_t* stage;            // kEpiStage: staging pool (records)
+  unsigned long long* stage_used;  // kEpiStage: pool chunk bump pointer (16-B units, zeroed by host)
+  uint64_t stage_cap16;      // kEpiStage: pool size in 16-B units
+  uint32_t* ovf_bits;        // kEpiStage: per item, set once its first warp failed to stage (zeroed by host)
+  uint32_t* ovf_items;       // kEpiStage / kEpiWrite: this launch's overflow queue (items)
+  uint32_t* ovf_n;           // kEpiStage / kEpiWrite: its length (zeroed by host)
+  const uint64_t* tile_offsets;  // kEpiWrite: exclusive prefix of the per-item counts (patterns in caller order)
   uint64_t* pos;             // kEpiWrite: output positions
   uint64_t cap;              // kEpiWrite: capacity of pos
-  uint64_t pos_offset;       // kEpiWrite: added to every written position (a shard's first owned position)
+  uint64_t pos_offset;       // kEpiStage / kEpiWrite: added to every position (a shard's first owned position)
+  unsigned long long* ctr;   // instrumented build (SMGPU_COUNTERS) only: device u64[kCounters], else unused
+};
+
+// Compare-step counters of the instrumented build (libsmgpu_counters.so, NEXT-2):
+enum Counter : int {
+  kCtrWarpTiles = 0,     // (warp, work item) pairs processed
+  kCtrBlocks = 1,        // BLOCK / PACKED: warp-blocks (512 CPL alignments) holding >= 1 valid alignment
+  kCtrSteps = 2,         // BLOCK / PACKED: SIMDcompare steps (peeled + ordered loop) executed in those blocks
+  kCtrChunks = 3,        // FILTER: 16-alignment chunks whose pi(1)-bytes were tested (phase A)
+  kCtrQueued = 4,        // FILTER: chunks holding p[pi(1)] (queued for phase B)
+  kCtrSurvivors = 5,     // FILTER: valid alignments matching pi(1) and pi(2) (entering verification)
+  kCtrVerify = 6,        // FILTER: pattern positions compared while verifying survivors
+  kCtrAlphaEff = 7,      // BLOCK / PACKED: alignments per warp-block (max)
+  kCounters = 8
 };
 
 // Kernel parameters: everything per launch, no __constant__ state, so launches on

@@ -46,7 +46,7 @@ cudaError_t launch_c(const HostLaunch& L, cudaStream_t st) {
 template <int STRAT>
 cudaError_t launch_strategy(const HostLaunch& L, cudaStream_t st) {
   if (L.epilogue == kEpiCount) return launch_c<STRAT, kEpiCount>(L, st);
-  if (L.epilogue == kEpiTileCount) return launch_c<STRAT, kEpiTileCount>(L, st);
+  if (L.epilogue == kEpiStage) return launch_c<STRAT, kEpiStage>(L, st);
   return launch_c<STRAT, kEpiWrite>(L, st);
 }
 

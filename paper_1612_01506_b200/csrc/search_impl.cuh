@@ -19,7 +19,8 @@
 //     then the pi-ordered loop with a warp-uniform exit test (__any_sync).
 //   * PACKED: BLOCK on 1- or 2-bit codes of the text bytes (small alphabets).
 //   * A6: popcount -> warp reduce -> one u64 atomic per warp and pattern.
-//   * A8: reporting writes ascending positions from a per-(pattern, tile) exclusive prefix.
+//   * A8: reporting stages each tile's matches (per-warp u16 lists / bitmaps) in one
+//     text pass; positions are expanded after a scan of the per-(pattern, tile) counts.
 #pragma once
 #include "device_util.cuh"
 #include "launch.h"
@@ -104,44 +105,57 @@ struct Pat {
   const uint32_t* tbl;  // this pattern's table in the kernel parameters (m entries, pi order; constant cache)
 };
 
+// Per-thread compare-step counters (search.cuh Counter); compiled to nothing unless
+// SMGPU_COUNTERS (the instrumented libsmgpu_counters.so).  Warp-uniform counters are
+// flushed from lane 0, per-lane ones from every lane.
+struct Ctr {
+#ifdef SMGPU_COUNTERS
+  unsigned long long v[kCounters] = {};
+  __device__ __forceinline__ void add(int i, unsigned long long x) { v[i] += x; }
+  __device__ __forceinline__ void flush(unsigned long long* out, int lane) {
+    if (!out) return;
+    for (int i = 0; i < kCounters; ++i) {
+      const bool uniform = i != kCtrSurvivors && i != kCtrVerify;
+      if (i == kCtrAlphaEff) {
+        if (lane == 0 && v[i]) atomicMax(out + i, v[i]);
+      } else if (v[i] && (!uniform || lane == 0)) {
+        atomicAdd(out + i, v[i]);
+      }
+    }
+  }
+#else
+  __device__ __forceinline__ void add(int, unsigned long long) {}
+  __device__ __forceinline__ void flush(unsigned long long*, int) {}
+#endif
+};
+
 // ---------------------------------------------------------------------------
-// This CTA's work items w = blockIdx.x + i * gridDim.x, in order.  For the write
-// epilogue (reporting pass 2) items of tiles without matches are skipped; a warp
-// probes 32 upcoming items at once (one load per lane + a ballot) instead of one
-// dependent load per item.  Every lane of the calling warp must call advance().
+// This CTA's work items (pattern k, tile ti), in order: w = blockIdx.x + i * gridDim.x
+// over the pattern-major item space; for kEpiWrite (reporting overflow pass) entries
+// blockIdx.x + i * gridDim.x of the launch's overflow queue instead.
 // ---------------------------------------------------------------------------
 template <int EPI, int CAP>
 struct WorkIter {
-  uint64_t next = blockIdx.x;  // next unprobed item
-  uint64_t base = 0;           // first item of the current probe
-  uint32_t mask = 0;           // non-empty items of the current probe not yet returned
-  // k0: pattern of the previously returned item (a lower bound for every later item)
-  __device__ __forceinline__ bool advance(const LaunchParams<CAP>& P, int lane, uint64_t& w, uint32_t k0) {
-    const uint64_t total = P.a.total_work, grid = gridDim.x;
-    if (EPI != kEpiWrite) {
-      if (next >= total) return false;
-      w = next;
-      next += grid;
-      return true;
+  uint64_t next = blockIdx.x;
+  uint64_t end;
+  uint32_t k = 0;
+  __device__ __forceinline__ explicit WorkIter(const LaunchParams<CAP>& P)
+      : end(EPI == kEpiWrite ? (uint64_t)*P.a.ovf_n : P.a.total_work) {}
+  __device__ __forceinline__ bool advance(const LaunchParams<CAP>& P, uint32_t& kk, uint64_t& ti) {
+    if (next >= end) return false;
+    if (EPI == kEpiWrite) {
+      const uint64_t item = P.a.ovf_items[next];
+      uint32_t j = 0;
+      while (j + 1 < P.a.npat && !(item >= P.d[j].item_base && item < P.d[j].item_base + P.d[j].ntiles)) ++j;
+      SMGPU_DCHECK(item >= P.d[j].item_base && item < P.d[j].item_base + P.d[j].ntiles);
+      kk = j;
+      ti = item - P.d[j].item_base;
+    } else {
+      while (next >= P.d[k].work_end) ++k;
+      kk = k;
+      ti = next - (P.d[k].work_end - P.d[k].ntiles);
     }
-    while (mask == 0) {
-      if (next >= total) return false;
-      base = next;
-      const uint64_t wj = base + (uint64_t)lane * grid;
-      bool nonempty = false;
-      if (wj < total) {
-        uint32_t kk = k0;
-        while (wj >= P.d[kk].work_end) ++kk;
-        const PatDesc& d = P.d[kk];
-        const uint64_t item = d.item_base + wj - (d.work_end - d.ntiles);
-        nonempty = P.a.tile_offsets[item + 1] != P.a.tile_offsets[item];
-      }
-      mask = __ballot_sync(0xFFFFFFFFu, nonempty);
-      next = base + 32 * grid;
-    }
-    const uint32_t j = __ffs(mask) - 1;
-    mask &= mask - 1;
-    w = base + (uint64_t)j * grid;
+    next += gridDim.x;
     return true;
   }
 };
@@ -152,20 +166,17 @@ struct WorkIter {
 // cp.async.bulk for the aligned interior, completion counted on full[s].
 // ---------------------------------------------------------------------------
 template <int EPI, int CAP>
-__device__ void produce(const LaunchParams<CAP>& P, uint8_t* ring, uint64_t* full, uint64_t* empty, int lane) {
+__device__ void produce(const LaunchParams<CAP>& P, uint8_t* ring, uint64_t* full, uint64_t* empty) {
   const LaunchArgs& a = P.a;
   const uint64_t pol = l2_policy_evict_first();
   const int64_t tlo = (int64_t)a.delta, thi = (int64_t)(a.delta + a.n);
   uint32_t s = 0, ph = 0;  // stage and its use parity
   bool wrapped = false;
-  uint32_t k = 0;
-  WorkIter<EPI, CAP> items;
-  uint64_t w;
-  while (items.advance(P, lane, w, k)) {
-    while (w >= P.d[k].work_end) ++k;
-    if (lane != 0) continue;  // lane 0 issues the copies; the warp only probes work items
+  WorkIter<EPI, CAP> items(P);
+  uint32_t k;
+  uint64_t ti;
+  while (items.advance(P, k, ti)) {
     const PatDesc& d = P.d[k];
-    const uint64_t ti = w - (d.work_end - d.ntiles);
     if (wrapped) mbar_wait_sleep(&empty[s], ph ^ 1u);  // consumers released this stage's previous use
     uint8_t* buf = ring + (size_t)s * a.stage_stride;
     const int64_t lo = (int64_t)((d.k_begin + ti) * a.tile) - (int64_t)d.pre;
@@ -213,13 +224,13 @@ __device__ __forceinline__ uint32_t compress_found(const Found4& F) {
 }
 __device__ __forceinline__ uint32_t gbit_to_alignment(uint32_t p) { return 4u * (7u - (p & 7u)) + (p >> 3); }
 
+// compressed found word -> 16-bit mask, bit (4i + k) <-> alignment 4i + k: byte k's
+// bit 7 of (g << i) is alignment 4i + k; the multiply gathers the four bit-7s of a
+// word into bits 28..31 (the shifted copies never overlap, so no carries)
 __device__ __forceinline__ uint32_t g_to_mask16(uint32_t g) {
   uint32_t m16 = 0;
-  while (g) {
-    const uint32_t p = __ffs(g) - 1;
-    g &= g - 1;
-    m16 |= 1u << gbit_to_alignment(p);
-  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) m16 |= ((((g << i) & 0x80808080u) * 0x00204081u) >> 28) << (4 * i);
   return m16;
 }
 
@@ -246,7 +257,7 @@ __device__ __forceinline__ uint32_t filter_entry(const Pat& pt, const uint8_t* b
 // survivors all lanes stay busy); survivors of long patterns still alive after
 // that are finished by the whole warp, one at a time, 32 positions of pi per step.
 __device__ __forceinline__ uint32_t verify_survivors(const Pat& pt, const uint8_t* buf, uint32_t c, uint32_t g,
-                                                     int lane) {
+                                                     int lane, Ctr& C) {
   const uint32_t qlane = pt.m < kLaneVerifyMaxM ? pt.m : kLaneVerifyMaxM;
   {
     uint32_t todo = g;
@@ -258,6 +269,7 @@ __device__ __forceinline__ uint32_t verify_survivors(const Pat& pt, const uint8_
       for (uint32_t q = 2; q < qlane; ++q) {
         const uint32_t e = pt.tbl[q];
         SMGPU_DCHECK((uint32_t)(xp - buf) + (e & 0xFFFFu) < pt.lim);
+        C.add(kCtrVerify, 1);
         if (xp[e & 0xFFFFu] != (e >> 16)) {
           g &= ~(1u << p);
           break;
@@ -285,6 +297,7 @@ __device__ __forceinline__ uint32_t verify_survivors(const Pat& pt, const uint8_
           const uint32_t e = pt.tbl[q];
           SMGPU_DCHECK((uint32_t)(xp - buf) + (e & 0xFFFFu) < pt.lim);
           mis = xp[e & 0xFFFFu] != (e >> 16);
+          C.add(kCtrVerify, 1);
         }
         if (__any_sync(0xFFFFFFFFu, mis)) {
           keep &= ~(1u << p);
@@ -355,15 +368,17 @@ struct CountSink {
 // per lane, all lanes busy.
 template <int Q, class Sink>
 __device__ __forceinline__ void filter_drain(const Pat& pt, const uint8_t* buf, int lane, const uint16_t* qc,
-                                             uint32_t qlen, bool edge, int32_t rlo, int32_t rhi, Sink& sink) {
+                                             uint32_t qlen, bool edge, int32_t rlo, int32_t rhi, Sink& sink,
+                                             Ctr& C) {
   for (uint32_t b0 = 0; b0 < qlen; b0 += 32) {
     const uint32_t i = b0 + lane;
     uint32_t c = 0, g = 0;
     if (i < qlen) {
       c = qc[i];
       g = filter_entry<Q>(pt, buf, c, edge, rlo, rhi);
+      C.add(kCtrSurvivors, __popc(g));
     }
-    if (pt.m >= 3) g = verify_survivors(pt, buf, c, g, lane);
+    if (pt.m >= 3) g = verify_survivors(pt, buf, c, g, lane, C);
     sink(c, g, lane);
   }
 }
@@ -373,7 +388,8 @@ __device__ __forceinline__ void filter_drain(const Pat& pt, const uint8_t* buf, 
 // queue (ascending chunk order); phase B (filter_drain) verifies them.
 template <int CPL, class Sink>
 __device__ __forceinline__ void filter_tile(const Pat& pt, const uint8_t* buf, uint32_t cw0, int lane, uint16_t* qc,
-                                            bool edge, int32_t rlo, int32_t rhi, Sink& sink) {
+                                            bool edge, int32_t rlo, int32_t rhi, Sink& sink, Ctr& C) {
+  C.add(kCtrChunks, 32u * CPL);
   constexpr int G = CPL < kGroup ? CPL : kGroup;
 #pragma unroll
   for (int g0 = 0; g0 < CPL; g0 += G) {
@@ -387,12 +403,13 @@ __device__ __forceinline__ void filter_tile(const Pat& pt, const uint8_t* buf, u
       if (hit) qc[qlen + __popc(bal & lanemask_lt())] = (uint16_t)c;
       qlen += __popc(bal);
     }
+    C.add(kCtrQueued, qlen);
     __syncwarp();
     switch ((pt.s2 >> 2) & 3u) {  // warp-uniform
-      case 0: filter_drain<0>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink); break;
-      case 1: filter_drain<1>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink); break;
-      case 2: filter_drain<2>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink); break;
-      default: filter_drain<3>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink); break;
+      case 0: filter_drain<0>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink, C); break;
+      case 1: filter_drain<1>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink, C); break;
+      case 2: filter_drain<2>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink, C); break;
+      default: filter_drain<3>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink, C); break;
     }
     __syncwarp();
   }
@@ -426,7 +443,7 @@ __device__ __forceinline__ void block_step(Found4 (&F)[CPL], const uint8_t* cbas
 // One warp's share of a BLOCK tile: Alg. 4 on 16 alignments per lane-chunk.
 template <int CPL>
 __device__ __forceinline__ void block_tile(const Pat& pt, const uint8_t* buf, uint32_t cw0, int lane, bool edge,
-                                           int32_t rlo, int32_t rhi, uint32_t* g_out) {
+                                           int32_t rlo, int32_t rhi, uint32_t* g_out, Ctr& C) {
   Found4 F[CPL];
 #pragma unroll
   for (int it = 0; it < CPL; ++it)
@@ -450,6 +467,10 @@ __device__ __forceinline__ void block_tile(const Pat& pt, const uint8_t* buf, ui
     block_step<CPL>(F, cbase, pt.tbl[k]);
   }
 #undef SMGPU_BLOCK_DCHECK
+  if (!edge || (rlo < (int32_t)(16u * cw0 + 512u * CPL) && rhi > (int32_t)(16u * cw0))) {  // a valid warp-block
+    C.add(kCtrBlocks, 1);
+    C.add(kCtrSteps, k);
+  }
 #pragma unroll
   for (int it = 0; it < CPL; ++it) g_out[it] = compress_found(F[it]);  // popcount of found
 }
@@ -547,7 +568,8 @@ __device__ __forceinline__ int packed_tile(const Pat& pt, const uint8_t* buf, ui
                                            uint32_t nchunks,
                                             uint32_t code_shift, uint32_t cw0, int warp, int lane, bool edge,
                                             int32_t rlo, int32_t rhi, uint64_t* empty_bar, uint32_t* m_out,
-                                            uint32_t* base_out) {
+                                            uint32_t* base_out, Ctr& C) {
+  const bool valid_block = !edge || (rlo < (int32_t)(16u * cw0 + 512u * CPL) && rhi > (int32_t)(16u * cw0));
 #pragma unroll
   for (int it = 0; it < CPL; ++it) {
     const uint32_t c = cw0 + it * 32u + lane;
@@ -600,6 +622,10 @@ __device__ __forceinline__ int packed_tile(const Pat& pt, const uint8_t* buf, ui
       if (!__any_sync(0xFFFFFFFFu, any != 0)) break;
       step(pt.tbl[k]);
     }
+    if (valid_block) {
+      C.add(kCtrBlocks, 1);
+      C.add(kCtrSteps, k);
+    }
 #pragma unroll
     for (int it = 0; it < D; ++it) {
       m_out[it] = F[it];
@@ -627,6 +653,10 @@ __device__ __forceinline__ int packed_tile(const Pat& pt, const uint8_t* buf, ui
     if (!__any_sync(0xFFFFFFFFu, any != 0)) break;
     packed_step<CPL, B>(F, W0, W1, pk32, qbase, lane, pt.tbl[k], pk_words);
   }
+  if (valid_block) {
+    C.add(kCtrBlocks, 1);
+    C.add(kCtrSteps, k);
+  }
 #pragma unroll
   for (int it = 0; it < CPL; ++it) {
     m_out[it] = B == 2 ? gather2(F[it]) : (F[it] & 0xFFFFu);
@@ -635,8 +665,9 @@ __device__ __forceinline__ int packed_tile(const Pat& pt, const uint8_t* buf, ui
   return CPL;
 }
 
-// Reporting: publish this warp's match count of tile w, wait for the CTA's other
-// compare warps, return the warp's first output index (tile offset + earlier warps).
+// Reporting (overflow pass): publish this warp's match count of item w, wait for the
+// CTA's other compare warps, return the warp's first output index (tile offset +
+// earlier warps).
 __device__ __forceinline__ uint64_t publish_and_offset(const LaunchArgs& a, uint32_t* s_wt, uint32_t par, int warp,
                                                        int lane, uint64_t w, uint32_t wtot) {
   if (lane == 0) s_wt[par * kConsumerWarps + warp] = wtot;
@@ -658,7 +689,7 @@ __device__ __forceinline__ void write_list(const LaunchArgs& a, const uint16_t* 
 // Reporting for strategies whose per-chunk results are still in registers.
 template <bool IN_G, int CPL>
 __device__ __forceinline__ void write_masks(const LaunchArgs& a, uint32_t* s_wt, uint16_t* list, uint32_t par,
-                                            int warp, int lane, uint64_t w, uint32_t cw0, int64_t x_base,
+                                            int warp, int lane, uint64_t w, uint32_t cw0, int64_t pos_base,
                                             const uint32_t (&mk)[CPL]) {
   AppendSink<IN_G> as{list};
 #pragma unroll
@@ -666,9 +697,9 @@ __device__ __forceinline__ void write_masks(const LaunchArgs& a, uint32_t* s_wt,
   const uint64_t run = publish_and_offset(a, s_wt, par, warp, lane, w, as.n);
   __syncwarp();
   if (as.n <= (uint32_t)kListCap) {
-    write_list(a, list, as.n, run, x_base - (int64_t)a.delta + (int64_t)a.pos_offset, lane);
+    write_list(a, list, as.n, run, pos_base, lane);
   } else {
-    WriteSink<IN_G> ws{run, x_base - (int64_t)a.delta + (int64_t)a.pos_offset, a.pos, a.cap};
+    WriteSink<IN_G> ws{run, pos_base, a.pos, a.cap};
 #pragma unroll
     for (int it = 0; it < CPL; ++it) ws(cw0 + it * 32u + lane, mk[it], lane);
   }
@@ -677,7 +708,7 @@ __device__ __forceinline__ void write_masks(const LaunchArgs& a, uint32_t* s_wt,
 // Reporting for PACKED: result units (mask, base) still in registers.
 template <int CPL>
 __device__ __forceinline__ void write_units(const LaunchArgs& a, uint32_t* s_wt, uint16_t* list, uint32_t par,
-                                            int warp, int lane, uint64_t w, int64_t x_base, const uint32_t (&mk)[CPL],
+                                            int warp, int lane, uint64_t w, int64_t pos_base, const uint32_t (&mk)[CPL],
                                             const uint32_t (&mbase)[CPL], int units) {
   AppendSink<false> as{list};
 #pragma unroll
@@ -686,13 +717,116 @@ __device__ __forceinline__ void write_units(const LaunchArgs& a, uint32_t* s_wt,
   const uint64_t run = publish_and_offset(a, s_wt, par, warp, lane, w, as.n);
   __syncwarp();
   if (as.n <= (uint32_t)kListCap) {
-    write_list(a, list, as.n, run, x_base - (int64_t)a.delta + (int64_t)a.pos_offset, lane);
+    write_list(a, list, as.n, run, pos_base, lane);
   } else {
-    WriteSink<false> ws{run, x_base - (int64_t)a.delta + (int64_t)a.pos_offset, a.pos, a.cap};
+    WriteSink<false> ws{run, pos_base, a.pos, a.cap};
 #pragma unroll
     for (int it = 0; it < CPL; ++it)
       if (it < units) ws.add(mbase[it], mk[it], lane);
   }
+}
+
+// Reporting pass 1 (kEpiStage): a warp's matches of a tile as per-chunk 16-bit masks
+// in its shared bitmap bm[i] (chunk cw0 + i, bit b <-> u = 16 (cw0 + i) + b); FILTER
+// writes only the chunks with matches, so its bitmap is kept clean between tiles.
+struct StageSink {
+  uint16_t* bm;
+  uint32_t cw0;
+  uint32_t n = 0;  // this lane's matches
+  __device__ __forceinline__ void operator()(uint32_t c, uint32_t g, int) {
+    if (g) {
+      bm[c - cw0] = (uint16_t)g_to_mask16(g);
+      n += __popc(g);
+    }
+  }
+};
+
+// Per-warp staging allocator: the warp owns a chunk of the pool and bump-allocates its
+// records from it, so a record costs no global round trip.  Lane 0's copy is used.
+struct StageAlloc {
+  unsigned long long next = 0, end = 0;  // 16-B units
+  // offset of `units` 16-B units followed by room for a terminator header, or
+  // ~0ull when the pool is exhausted
+  __device__ __forceinline__ unsigned long long take(const LaunchArgs& a, uint32_t units) {
+    if (next + units + 1 > end) {
+      const unsigned long long c = atomicAdd(a.stage_used, (unsigned long long)kStageChunk);
+      if (c >= a.stage_cap16) return ~0ull;
+      next = c;
+      end = c + kStageChunk < a.stage_cap16 ? c + kStageChunk : a.stage_cap16;
+      if (next + units + 1 > end) return ~0ull;  // the pool's last, partial chunk is too small
+    }
+    const unsigned long long o = next;
+    next += units;  // the terminator slot is reused by the next record
+    return o;
+  }
+};
+
+// Reporting pass 1, one warp with wcnt > 0 matches in work item `item`: post its count
+// (wc, per-pattern total), then write its record -- the ascending u16 list of
+// tile-relative alignments when sparse, its bitmap when dense -- followed by a zero
+// terminator header.  No other warp is waited for.  If the pool is exhausted the item
+// is queued (once) for the overflow pass, which recomputes it from the text.
+template <int CPL, bool CLEAN>
+__device__ __forceinline__ void stage_warp(const LaunchArgs& a, const PatDesc& d, uint16_t* bm, StageAlloc& al,
+                                           int warp, int lane, uint64_t item, int64_t pos_base, uint32_t wcnt) {
+  constexpr uint32_t kWspan = 512u * CPL;  // alignments per warp (32 lanes x CPL chunks x 16)
+  constexpr uint32_t kLog2Cpl = CPL == 8 ? 3 : CPL == 4 ? 2 : CPL == 2 ? 1 : 0;
+  const uint32_t dbytes = rec_warp_bytes(wcnt, kWspan);
+  unsigned long long o = 0;
+  if (lane == 0) {
+    a.wc[item * kConsumerWarps + warp] = (uint16_t)wcnt;
+    atomicAdd(reinterpret_cast<unsigned long long*>(d.count_out), (unsigned long long)wcnt);
+    o = al.take(a, 1u + dbytes / 16u);
+    if (o == ~0ull && !(atomicOr(&a.ovf_bits[item >> 5], 1u << (item & 31)) & (1u << (item & 31))))
+      a.ovf_items[atomicAdd(a.ovf_n, 1u)] = (uint32_t)item;
+  }
+  o = __shfl_sync(0xFFFFFFFFu, o, 0);
+  if (o != ~0ull) {
+    uint8_t* rec = a.stage + o * 16u;
+    if (lane == 0) {
+      uint4 h;
+      h.x = (uint32_t)(uint64_t)pos_base;
+      h.y = (uint32_t)((uint64_t)pos_base >> 32);
+      h.z = (uint32_t)item;
+      h.w = wcnt | ((uint32_t)warp << 16) | (kLog2Cpl << 24);
+      reinterpret_cast<uint4*>(rec)[0] = h;
+      reinterpret_cast<uint4*>(rec + kRecHeader + dbytes)[0] = make_uint4(0u, 0u, 0u, 0u);  // terminator
+    }
+    if (2u * wcnt < kWspan / 8u) {  // sparse: ascending u16 list (lane l owns chunks [l CPL, l CPL + CPL))
+      uint16_t mk[CPL];
+      uint32_t pc = 0;
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {
+        mk[j] = bm[lane * CPL + j];
+        pc += __popc((uint32_t)mk[j]);
+      }
+      const uint32_t incl = warp_incl_scan(pc, lane);
+      uint32_t idx = incl - pc;
+      uint16_t* L = reinterpret_cast<uint16_t*>(rec + kRecHeader);
+      const uint32_t u0 = (uint32_t)warp * kWspan + 16u * (uint32_t)lane * CPL;
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {
+        uint32_t m = mk[j];
+        while (m) {
+          const uint32_t b = __ffs(m) - 1;
+          m &= m - 1;
+          L[idx++] = (uint16_t)(u0 + 16u * j + b);
+        }
+      }
+    } else {  // dense: the bitmap (64 CPL bytes)
+      const uint4* src = reinterpret_cast<const uint4*>(bm);
+      uint4* dst = reinterpret_cast<uint4*>(rec + kRecHeader);
+#pragma unroll
+      for (uint32_t i = lane; i < 4u * CPL; i += 32) dst[i] = src[i];
+    }
+  }
+  if (CLEAN) {  // FILTER's bitmap must be clean for the next tile
+    __syncwarp();
+    uint32_t* bw = reinterpret_cast<uint32_t*>(bm);
+#pragma unroll
+    for (uint32_t i = lane; i < 16u * CPL; i += 32) bw[i] = 0u;
+  }
+  __syncwarp();
 }
 
 }  // namespace
@@ -722,66 +856,81 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
   __syncthreads();
 
   if (warp == kConsumerWarps) {
-    if (EPI == kEpiWrite) produce<EPI>(P, ring, full, empty, lane);  // the warp probes work items
-    else if (lane == 0) produce<EPI>(P, ring, full, empty, lane);
+    if (lane == 0) produce<EPI>(P, ring, full, empty);
     return;
   }
 
   uint16_t* qc = reinterpret_cast<uint16_t*>(smem + kQueueOff) + warp * kQueueLen;
-  uint16_t* list = reinterpret_cast<uint16_t*>(smem + a.list_off) + warp * kListCap;  // reporting only
+  // reporting only: kEpiWrite position list (kListCap u16) / kEpiStage bitmap (32 CPL u16)
+  uint16_t* list = reinterpret_cast<uint16_t*>(smem + a.list_off) + warp * kListCap;
+  StageAlloc salloc;     // kEpiStage: this warp's staging-pool chunk
+  if (EPI == kEpiStage) {  // the bitmap starts clean
+    uint32_t* bw = reinterpret_cast<uint32_t*>(list);
+    for (uint32_t i = lane; i < 16u * CPL; i += 32) bw[i] = 0u;
+    __syncwarp();
+  }
   const uint32_t T = a.tile;
   const uint32_t cw0 = (uint32_t)warp * 32u * CPL;  // first chunk of this warp
   uint32_t s = 0, ph = 0, par = 0, par_pk = 0;
-  uint32_t k = 0;
-  uint32_t acc = 0;  // kEpiCount: this lane's matches of pattern k so far
-  WorkIter<EPI, CAP> items;
-  uint64_t w;
-  while (items.advance(P, lane, w, k)) {
-    while (w >= P.d[k].work_end) {
-      if (EPI == kEpiCount) {  // flush pattern k (warp-uniform)
-        const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, acc);
-        if (lane == 0 && ws) atomicAdd(reinterpret_cast<unsigned long long*>(P.d[k].count_out), (unsigned long long)ws);
-        acc = 0;
-      }
-      ++k;
+  uint32_t kc = 0;   // kEpiCount: pattern whose matches `acc` holds
+  uint32_t acc = 0;  // kEpiCount: this lane's matches of pattern kc so far
+  Ctr C;
+#ifdef SMGPU_COUNTERS
+  C.v[kCtrAlphaEff] = (STRAT == kFilter) ? 0ull : 512ull * CPL;
+#endif
+  WorkIter<EPI, CAP> items(P);
+  uint32_t k;
+  uint64_t ti;
+  while (items.advance(P, k, ti)) {
+    C.add(kCtrWarpTiles, 1);
+    if (EPI == kEpiCount && k != kc) {  // flush pattern kc (warp-uniform; k only grows here)
+      const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, acc);
+      if (lane == 0 && ws) atomicAdd(reinterpret_cast<unsigned long long*>(P.d[kc].count_out), (unsigned long long)ws);
+      acc = 0;
+      kc = k;
     }
     const PatDesc& d = P.d[k];
-    const uint64_t ti = w - (d.work_end - d.ntiles);
+    const uint64_t item = d.item_base + ti;
     mbar_wait(&full[s], ph);
     const uint8_t* buf = ring + (size_t)s * a.stage_stride;
     const Pat pt{d.m, d.r, d.a1, d.bc1, d.s2, d.bc2, d.pre, d.stage_len, P.e + d.tbl};
     const bool edge = ti < d.edge_lo || ti >= d.edge_hi;  // tile holds invalid alignments
     const int64_t shift = (STRAT == kFilter) ? (int64_t)d.a1 : 0;
     const int64_t x_base = (int64_t)((d.k_begin + ti) * T) - shift;  // alignment offset of u = 0
+    const int64_t pos_base = x_base - (int64_t)a.delta + (int64_t)a.pos_offset;  // position of u = 0
     int32_t rlo = 0, rhi = (int32_t)T;
     if (edge) {
       const int64_t vlo = (int64_t)a.delta, vhi = (int64_t)(a.delta + d.A);
       rlo = (int32_t)imin(imax(vlo - x_base, 0), (int64_t)T);
       rhi = (int32_t)imin(imax(vhi - x_base, 0), (int64_t)T);
     }
+    bool released = false;  // the stage's bytes were handed back to the producer
 
     if (STRAT == kFilter) {
-      if (EPI != kEpiWrite) {
+      if (EPI == kEpiCount) {
         CountSink cs;
-        filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, cs);
-        if (EPI == kEpiCount) {
-          acc += cs.n;
-        } else {
-          const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, cs.n);
-          if (lane == 0 && ws) {
-            atomicAdd(reinterpret_cast<unsigned long long*>(&a.tile_counts[d.item_base + ti]), (unsigned long long)ws);
-            atomicAdd(reinterpret_cast<unsigned long long*>(d.count_out), (unsigned long long)ws);
-          }
-        }
-      } else {  // buffer this warp's matches, exchange warp totals, write coalesced
+        filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, cs, C);
+        acc += cs.n;
+      } else if (EPI == kEpiStage) {
+        StageSink sk{list, cw0};
+        filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, sk, C);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        released = true;
+        const uint32_t wcnt = __reduce_add_sync(0xFFFFFFFFu, sk.n);
+        if (wcnt) stage_warp<CPL, true>(a, d, list, salloc, warp, lane, item, pos_base, wcnt);
+      } else {  // overflow pass: buffer this warp's matches, exchange warp totals, write coalesced
         AppendSink<true> as{list};
-        filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, as);
-        uint64_t run = publish_and_offset(a, s_wt, par, warp, lane, d.item_base + ti, as.n);
+        filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, as, C);
+        uint64_t run = publish_and_offset(a, s_wt, par, warp, lane, item, as.n);
         if (as.n <= (uint32_t)kListCap) {
-          write_list(a, list, as.n, run, x_base - (int64_t)a.delta + (int64_t)a.pos_offset, lane);
+          write_list(a, list, as.n, run, pos_base, lane);
         } else {  // list overflow (very dense tile): ranked writes from a recomputation
-          WriteSink<> ws{run, x_base - (int64_t)a.delta + (int64_t)a.pos_offset, a.pos, a.cap};
-          filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, ws);
+          WriteSink<> ws{run, pos_base, a.pos, a.cap};
+          {
+            Ctr C2;  // a recomputation: not counted again
+            filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, ws, C2);
+          }
         }
         par ^= 1u;
       }
@@ -790,7 +939,8 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
       uint32_t mk[CPL], mbase[CPL];
       uint8_t* pk = smem + a.pack_off + par_pk * a.pack_bytes;
       const int units = packed_tile<CPL, B>(pt, buf, pk, a.pack_bytes / 4u, d.stage_len / 16u, a.code_shift, cw0,
-                                            warp, lane, edge, rlo, rhi, &empty[s], mk, mbase);
+                                            warp, lane, edge, rlo, rhi, &empty[s], mk, mbase, C);
+      released = true;  // packed_tile released the stage after packing
       par_pk ^= 1u;
       uint32_t tc = 0;
 #pragma unroll
@@ -798,38 +948,51 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
         if (it < units) tc += __popc(mk[it]);
       if (EPI == kEpiCount) {
         acc += tc;
-      } else if (EPI == kEpiTileCount) {
-        const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, tc);
-        if (lane == 0 && ws) {
-          atomicAdd(reinterpret_cast<unsigned long long*>(&a.tile_counts[d.item_base + ti]), (unsigned long long)ws);
-          atomicAdd(reinterpret_cast<unsigned long long*>(d.count_out), (unsigned long long)ws);
+      } else if (EPI == kEpiStage) {
+        constexpr bool kWide = B == 1 && CPL >= 2;  // 32-bit masks of 32 alignments
+        const uint32_t wcnt = __reduce_add_sync(0xFFFFFFFFu, tc);
+        if (wcnt) {
+#pragma unroll
+          for (int it = 0; it < CPL; ++it) {
+            if (it >= units) break;
+            const uint32_t rel = mbase[it] / 16u - cw0;  // chunk index within the warp
+            if (kWide) reinterpret_cast<uint32_t*>(list)[rel / 2u] = mk[it];
+            else list[rel] = (uint16_t)mk[it];
+          }
+          __syncwarp();
+          stage_warp<CPL, false>(a, d, list, salloc, warp, lane, item, pos_base, wcnt);
         }
       } else {
-        write_units<CPL>(a, s_wt, list, par, warp, lane, d.item_base + ti, x_base, mk, mbase, units);
+        write_units<CPL>(a, s_wt, list, par, warp, lane, item, pos_base, mk, mbase, units);
         par ^= 1u;
       }
     } else {
       uint32_t g[CPL];
-      block_tile<CPL>(pt, buf, cw0, lane, edge, rlo, rhi, g);
+      block_tile<CPL>(pt, buf, cw0, lane, edge, rlo, rhi, g, C);
       uint32_t tc = 0;
 #pragma unroll
       for (int it = 0; it < CPL; ++it) tc += __popc(g[it]);
       if (EPI == kEpiCount) {
         acc += tc;
-      } else if (EPI == kEpiTileCount) {
-        const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, tc);
-        if (lane == 0 && ws) {
-          atomicAdd(reinterpret_cast<unsigned long long*>(&a.tile_counts[d.item_base + ti]), (unsigned long long)ws);
-          atomicAdd(reinterpret_cast<unsigned long long*>(d.count_out), (unsigned long long)ws);
+      } else if (EPI == kEpiStage) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        released = true;
+        const uint32_t wcnt = __reduce_add_sync(0xFFFFFFFFu, tc);
+        if (wcnt) {
+#pragma unroll
+          for (int it = 0; it < CPL; ++it) list[it * 32 + lane] = (uint16_t)g_to_mask16(g[it]);
+          __syncwarp();
+          stage_warp<CPL, false>(a, d, list, salloc, warp, lane, item, pos_base, wcnt);
         }
       } else {
-        write_masks<true, CPL>(a, s_wt, list, par, warp, lane, d.item_base + ti, cw0, x_base, g);
+        write_masks<true, CPL>(a, s_wt, list, par, warp, lane, item, cw0, pos_base, g);
         par ^= 1u;
       }
     }
 
     __syncwarp();
-    if (STRAT != kPacked1 && STRAT != kPacked2 && lane == 0) mbar_arrive(&empty[s]);  // PACKED released it after packing
+    if (!released && lane == 0) mbar_arrive(&empty[s]);
     if (++s == a.stages) {
       s = 0;
       ph ^= 1u;
@@ -838,8 +1001,9 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
 
   if (EPI == kEpiCount) {
     const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, acc);
-    if (lane == 0 && ws) atomicAdd(reinterpret_cast<unsigned long long*>(P.d[k].count_out), (unsigned long long)ws);
+    if (lane == 0 && ws) atomicAdd(reinterpret_cast<unsigned long long*>(P.d[kc].count_out), (unsigned long long)ws);
   }
+  C.flush(a.ctr, lane);
 }
 
 }  // namespace smgpu

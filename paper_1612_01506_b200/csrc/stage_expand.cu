@@ -1,0 +1,152 @@
+// stage_expand.cu -- reporting (A8, "printing position i"): turn the
+// staged match records of reporting pass 1 (kEpiStage, search.cuh / search_impl.cuh)
+// into ascending 0-based positions.  The matches of compare warp w in work item
+// `item` go to pos[tile_offsets[item] + sum_{w' < w} wc[item][w'] ..): items in the
+// scanned (pattern-major, tile-ascending) order, warps ascending within an item,
+// alignments ascending within a warp -- the order of Alg. 1's loop.
+// Only the staging pool is read, never the text.
+//
+// One warp per pool chunk (16 KiB): the chunk is pulled into shared memory with
+// independent 16-B loads, lane 0 walks its record chain (up to the zero terminator),
+// the lanes fetch the records' output offsets in parallel, then each record is
+// written: u16 lists lane-parallel, bitmaps 32 x 32 alignments per round through a
+// shared index buffer, so that the 8-byte position stores are coalesced.
+#include "device_util.cuh"
+#include "launch.h"
+
+namespace smgpu {
+namespace {
+
+constexpr int kExpandWarps = 4;
+constexpr uint32_t kChunkBytes = kStageChunk * 16u;
+constexpr uint32_t kMaxRecs = kStageChunk / 2u;  // a record is >= 2 units (header + data)
+constexpr uint32_t kWarpSmem = kChunkBytes + kMaxRecs * (8u + 2u) + 2048u;
+
+__device__ __forceinline__ uint32_t warp_incl_scan_x(uint32_t v, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, v, d);
+    if (lane >= d) v += u;
+  }
+  return v;
+}
+
+__device__ __forceinline__ void write_record(const uint8_t* rec, uint64_t out, uint64_t* pos, uint64_t cap,
+                                             uint16_t* sbuf, int lane) {
+  const uint4 h = *reinterpret_cast<const uint4*>(rec);
+  const int64_t pos_base = (int64_t)(((uint64_t)h.y << 32) | h.x);
+  const uint32_t c = h.w & 0xFFFFu, w = (h.w >> 16) & 0xFFu;
+  const uint32_t wspan = 512u << (h.w >> 24);
+  const uint8_t* data = rec + kRecHeader;
+  if (2u * c < wspan / 8u) {  // u16 list
+    const uint16_t* L = reinterpret_cast<const uint16_t*>(data);
+    for (uint32_t i = lane; i < c; i += 32)
+      if (out + i < cap) pos[out + i] = (uint64_t)(pos_base + (int64_t)L[i]);
+    return;
+  }
+  // bitmap: bit b of u32 word i <-> u = w wspan + 32 i + b
+  const uint32_t* bm = reinterpret_cast<const uint32_t*>(data);
+  const uint32_t words = wspan / 32u;
+  uint64_t o = out;
+  for (uint32_t r0 = 0; r0 < words && o < cap; r0 += 32) {
+    const uint32_t i = r0 + lane;
+    uint32_t mk = i < words ? bm[i] : 0u;
+    const uint32_t pc = __popc(mk);
+    const uint32_t incl = warp_incl_scan_x(pc, lane);
+    const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    if (tot == 0) continue;
+    uint32_t j = incl - pc;
+    const uint32_t u0 = w * wspan + 32u * i;
+    while (mk) {
+      const uint32_t b = __ffs(mk) - 1;
+      mk &= mk - 1;
+      sbuf[j++] = (uint16_t)(u0 + b);
+    }
+    __syncwarp();
+    for (uint32_t q = lane; q < tot; q += 32)
+      if (o + q < cap) pos[o + q] = (uint64_t)(pos_base + (int64_t)sbuf[q]);
+    __syncwarp();
+    o += tot;
+  }
+}
+
+__global__ void __launch_bounds__(kExpandWarps * 32) stage_expand_kernel(const uint8_t* stage,
+                                                                        const unsigned long long* stage_used,
+                                                                        uint64_t cap16, const uint16_t* wc,
+                                                                        const uint64_t* tile_offsets, uint64_t* pos,
+                                                                        uint64_t cap) {
+  extern __shared__ __align__(16) uint8_t xsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* cbuf = xsm + warp * kWarpSmem;                                    // the chunk
+  uint64_t* rout = reinterpret_cast<uint64_t*>(cbuf + kChunkBytes);           // [kMaxRecs] output offsets
+  uint16_t* roff = reinterpret_cast<uint16_t*>(rout + kMaxRecs);              // [kMaxRecs] record offsets (units)
+  uint16_t* sbuf = roff + kMaxRecs;                                           // [1024] bitmap expansion
+  const unsigned long long used = *stage_used < cap16 ? *stage_used : cap16;
+  const uint64_t nchunks = (used + kStageChunk - 1) / kStageChunk;
+  const uint64_t gw = (uint64_t)blockIdx.x * kExpandWarps + warp, nw = (uint64_t)gridDim.x * kExpandWarps;
+  for (uint64_t ch = gw; ch < nchunks; ch += nw) {
+    const uint64_t base16 = ch * kStageChunk;
+    const uint32_t len16 = (uint32_t)(cap16 - base16 < kStageChunk ? cap16 - base16 : kStageChunk);
+    const uint4* src = reinterpret_cast<const uint4*>(stage + base16 * 16u);
+    uint4* dst = reinterpret_cast<uint4*>(cbuf);
+#pragma unroll 8
+    for (uint32_t i = lane; i < len16; i += 32) dst[i] = src[i];
+    __syncwarp();
+    uint32_t nrec = 0;
+    if (lane == 0) {  // walk the chain of records up to the terminator (or the chunk's end)
+      uint32_t o = 0;
+      while (o < len16) {
+        const uint32_t hw = reinterpret_cast<const uint32_t*>(cbuf + o * 16u)[3];
+        const uint32_t c = hw & 0xFFFFu;
+        if (c == 0) break;
+        roff[nrec++] = (uint16_t)o;
+        o += 1u + rec_warp_bytes(c, 512u << (hw >> 24)) / 16u;
+      }
+    }
+    nrec = __shfl_sync(0xFFFFFFFFu, nrec, 0);
+    __syncwarp();
+    for (uint32_t r = lane; r < nrec; r += 32) {  // output offset of each record
+      const uint4 h = *reinterpret_cast<const uint4*>(cbuf + roff[r] * 16u);
+      const uint64_t item = h.z;
+      const uint32_t w = (h.w >> 16) & 0xFFu;
+      const uint4 v = reinterpret_cast<const uint4*>(wc)[item];
+      const uint32_t cw[8] = {v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16,
+                              v.z & 0xFFFFu, v.z >> 16, v.w & 0xFFFFu, v.w >> 16};
+      uint64_t pre = 0;
+#pragma unroll
+      for (uint32_t q = 0; q < 8; ++q)
+        if (q < w) pre += cw[q];
+      rout[r] = tile_offsets[item] + pre;
+    }
+    __syncwarp();
+    for (uint32_t r = 0; r < nrec; ++r) {
+      const uint64_t out = rout[r];
+      if (out < cap) write_record(cbuf + roff[r] * 16u, out, pos, cap, sbuf, lane);
+    }
+    __syncwarp();  // cbuf / rout are reused for the next chunk
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_stage_expand(const uint8_t* stage, const unsigned long long* stage_used, uint64_t stage_cap16,
+                                const uint16_t* wc, const uint64_t* tile_offsets, uint64_t* pos, uint64_t cap,
+                                int num_sms, cudaStream_t st) {
+  if (stage_cap16 == 0) return cudaSuccess;
+  const size_t smem = (size_t)kExpandWarps * kWarpSmem;
+  static bool attr = false;  // benign race: idempotent
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(stage_expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const uint64_t max_chunks = (stage_cap16 + kStageChunk - 1) / kStageChunk;
+  const uint64_t want = (max_chunks + kExpandWarps - 1) / kExpandWarps;
+  const uint64_t lim = (uint64_t)num_sms * 2;  // 2 CTAs of 4 warps per SM (shared memory)
+  const int grid = (int)(want < lim ? want : lim);
+  stage_expand_kernel<<<grid, kExpandWarps * 32, smem, st>>>(stage, stage_used, stage_cap16, wc, tile_offsets, pos,
+                                                             cap);
+  return cudaGetLastError();
+}
+
+}  // namespace smgpu

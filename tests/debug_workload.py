@@ -9,10 +9,10 @@ import oracle
 import paper_1612_01506_b200 as sm
 
 torch.cuda.set_device(0)
-print("library:", sm.load_library()._name)
+print("library:", sm.load_library()._name, "SMGPU_STAGE_BYTES:", os.environ.get("SMGPU_STAGE_BYTES"))
 rng = np.random.default_rng(2024)
 fails = 0
-for alpha in (b"ACGT", b"\x00\x01", bytes(range(32, 127))):
+for alpha in (b"ACGT", b"\x00\x01", bytes(range(32, 127)), b"a"):
     syms = np.frombuffer(alpha, dtype=np.uint8)
     for n in (5, 31, 4100, 70003):
         a = syms[rng.integers(0, syms.size, n)]

@@ -152,7 +152,19 @@ def test_c4_periodic_closed_forms(sm):
     d = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
     sm.sm_count_batch(pats, t, d)
     assert d.cpu().tolist() == [c["count"] for c in g["cases"]]
-    del t
+    # NEXT-1 dense reporting: p = a^17 occurs at every alignment 0 .. n - 17 (2^30 - 16
+    # positions, 8 GiB of output); positions are unique, so compare them all, in slices
+    m = 17
+    want = spec.n - m + 1
+    pos = torch.empty(want, dtype=torch.int64, device="cuda")
+    d1 = torch.zeros(1, dtype=torch.int64, device="cuda")
+    sm.sm_report_batch([b"a" * m], t, pos, d1)
+    assert int(d1.item()) == want
+    step = 1 << 27
+    for lo in range(0, want, step):
+        hi = min(want, lo + step)
+        assert torch.equal(pos[lo:hi], torch.arange(lo, hi, dtype=torch.int64, device="cuda")), lo
+    del pos, t
     _free()
 
 

@@ -203,6 +203,65 @@ def test_alg4_absent_symbol_compare_bound():
             assert ncmp == -(-(len(t) - 4 + 1) // alpha) * r
 
 
+# --------------------------------------------------------------------------- Alg. 4 compare counts (NEXT-2)
+def test_alg4_steps_equals_alg4_compares_small_alpha():
+    """oracle_alg4_steps (found as one flag per alignment, any alpha) executes exactly the
+    SIMDcompare calls of oracle_alg4_count (found as a 64-bit mask, alpha <= 64)."""
+    rng = np.random.default_rng(41)
+    for trial in range(300):
+        sigma = int(rng.choice([1, 2, 4, 20, 256]))
+        n = int(rng.integers(0, 400))
+        m = int(rng.integers(1, 20))
+        t = rng.integers(0, sigma, n, dtype=np.uint8).tobytes()
+        if n >= m and rng.random() < 0.7:
+            s0 = int(rng.integers(0, n - m + 1))
+            p = t[s0:s0 + m]
+        else:
+            p = rng.integers(0, sigma, m, dtype=np.uint8).tobytes()
+        alpha = int(rng.choice([1, 3, 8, 16, 32, 64]))
+        pi = rng.permutation(m).astype(np.uint32)
+        r = int(rng.integers(1, m + 3))
+        _, ncmp = oracle.alg4_count(p, t, alpha=alpha, pi=pi, r=r)
+        steps, blocks = oracle.alg4_steps(p, t, alpha=alpha, pi=pi, r=r)
+        assert steps == ncmp, dict(trial=trial)
+        assert blocks == (-(-(n - m + 1) // alpha) if n >= m else 0)
+
+
+def test_alg4_steps_closed_forms():
+    # t = a^n, p = a^m: no alignment ever fails, every block runs all m compares
+    for n, m, alpha in ((5000, 7, 512), (4096, 1, 4096), (9999, 33, 1000), (70, 70, 4096)):
+        steps, blocks = oracle.alg4_steps(b"a" * m, b"a" * n, alpha=alpha, r=2)
+        nb = -(-(n - m + 1) // alpha)
+        assert blocks == nb and steps == nb * m
+    # a symbol absent from t compared first: every block stops after the r peeled compares
+    t = bytes(np.random.default_rng(3).integers(0, 4, 20000, dtype=np.uint8))
+    p = bytes([1, 2, 9, 3, 0])
+    pi = oracle.order(oracle.hist(t), p)
+    for alpha in (100, 512, 4096):
+        for r in (1, 2, 4):
+            steps, blocks = oracle.alg4_steps(p, t, alpha=alpha, pi=pi, r=r)
+            assert steps == -(-(len(t) - 5 + 1) // alpha) * r
+
+
+def test_alg4_steps_alpha1_is_scalar_naive_compares():
+    """alpha = 1, identity order, r = 1: the character comparisons of Alg. 1,
+    counted by brute force -- the paper's compares-per-alignment statistic."""
+    rng = np.random.default_rng(8)
+    for trial in range(60):
+        n = int(rng.integers(1, 200))
+        m = int(rng.integers(1, 8))
+        t = rng.integers(0, int(rng.choice([2, 3, 26])), n, dtype=np.uint8).tobytes()
+        p = rng.integers(0, 3, m, dtype=np.uint8).tobytes()
+        want = 0
+        for i in range(n - m + 1):
+            for j in range(m):
+                want += 1
+                if t[i + j] != p[j]:
+                    break
+        steps, blocks = oracle.alg4_steps(p, t, alpha=1, r=1)
+        assert steps == want and blocks == max(0, n - m + 1)
+
+
 # --------------------------------------------------------------------------- pi_h
 def test_pi_h_golden_and_permutation():
     g = json.load(open(os.path.join(GOLD, "pi_h.json")))
