@@ -359,7 +359,9 @@ def sm_launch_count() -> int:
 def sm_counters(reset: bool = False) -> dict:
     """Compare-step counters of the instrumented build (SMGPU_LIB=counters), see smgpu.h."""
     out = np.zeros(8, dtype=np.uint64)
-    _raise(load_library().sm_counters(out.ctypes.data, int(reset)))
+    s = load_library().sm_counters(out.ctypes.data, int(reset))
+    if s:
+        _raise(s)
     return {k: int(v) for k, v in zip(COUNTER_NAMES, out)}
 
 

@@ -44,7 +44,7 @@ enum Epilogue : int { kEpiCount = 0, kEpiStage = 1, kEpiWrite = 2 };
 // and posts cnt into wc[item][warp] (u16 x 8 per item, zero-initialised): the scan of
 // the per-item sums gives each item's output offset, wc its warps' order inside it.
 constexpr uint32_t kRecHeader = 16;
-constexpr uint32_t kStageChunk = 1024;  // 16-B units (16 KiB) >= largest record + terminator
+constexpr uint32_t kStageChunk = 512;   // 16-B units (8 KiB) >= largest record (528 B) + terminator
 __host__ __device__ inline uint32_t rec_warp_bytes(uint32_t cnt, uint32_t wspan) {
   if (cnt == 0) return 0;
   return 2u * cnt < wspan / 8u ? ((2u * cnt + 15u) & ~15u) : wspan / 8u;

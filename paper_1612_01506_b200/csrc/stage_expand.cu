@@ -6,7 +6,7 @@
 // alignments ascending within a warp -- the order of Alg. 1's loop.
 // Only the staging pool is read, never the text.
 //
-// One warp per pool chunk (16 KiB): the chunk is pulled into shared memory with
+// One warp per pool chunk (8 KiB): the chunk is pulled into shared memory with
 // independent 16-B loads, lane 0 walks its record chain (up to the zero terminator),
 // the lanes fetch the records' output offsets in parallel, then each record is
 // written: u16 lists lane-parallel, bitmaps 32 x 32 alignments per round through a
@@ -17,7 +17,7 @@
 namespace smgpu {
 namespace {
 
-constexpr int kExpandWarps = 4;
+constexpr int kExpandWarps = 8;
 constexpr uint32_t kChunkBytes = kStageChunk * 16u;
 constexpr uint32_t kMaxRecs = kStageChunk / 2u;  // a record is >= 2 units (header + data)
 constexpr uint32_t kWarpSmem = kChunkBytes + kMaxRecs * (8u + 2u) + 2048u;
@@ -105,18 +105,34 @@ __global__ void __launch_bounds__(kExpandWarps * 32) stage_expand_kernel(const u
     }
     nrec = __shfl_sync(0xFFFFFFFFu, nrec, 0);
     __syncwarp();
-    for (uint32_t r = lane; r < nrec; r += 32) {  // output offset of each record
-      const uint4 h = *reinterpret_cast<const uint4*>(cbuf + roff[r] * 16u);
-      const uint64_t item = h.z;
-      const uint32_t w = (h.w >> 16) & 0xFFu;
-      const uint4 v = reinterpret_cast<const uint4*>(wc)[item];
-      const uint32_t cw[8] = {v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16,
-                              v.z & 0xFFFFu, v.z >> 16, v.w & 0xFFFFu, v.w >> 16};
-      uint64_t pre = 0;
+    // output offset of each record: lane l takes records l, l + 32, ..., four at a time so
+    // that four independent pairs of global loads are in flight
+    for (uint32_t r0 = lane; r0 < nrec; r0 += 128) {
+      uint4 v[4];
+      uint64_t off[4];
+      uint32_t wv[4];
 #pragma unroll
-      for (uint32_t q = 0; q < 8; ++q)
-        if (q < w) pre += cw[q];
-      rout[r] = tile_offsets[item] + pre;
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t r = r0 + 32u * u;
+        if (r < nrec) {
+          const uint4 h = *reinterpret_cast<const uint4*>(cbuf + roff[r] * 16u);
+          wv[u] = (h.w >> 16) & 0xFFu;
+          v[u] = reinterpret_cast<const uint4*>(wc)[h.z];
+          off[u] = tile_offsets[h.z];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t r = r0 + 32u * u;
+        if (r >= nrec) break;
+        const uint32_t cw[8] = {v[u].x & 0xFFFFu, v[u].x >> 16, v[u].y & 0xFFFFu, v[u].y >> 16,
+                                v[u].z & 0xFFFFu, v[u].z >> 16, v[u].w & 0xFFFFu, v[u].w >> 16};
+        uint64_t pre = 0;
+#pragma unroll
+        for (uint32_t q = 0; q < 8; ++q)
+          if (q < wv[u]) pre += cw[q];
+        rout[r] = off[u] + pre;
+      }
     }
     __syncwarp();
     for (uint32_t r = 0; r < nrec; ++r) {
@@ -142,7 +158,7 @@ cudaError_t launch_stage_expand(const uint8_t* stage, const unsigned long long* 
   }
   const uint64_t max_chunks = (stage_cap16 + kStageChunk - 1) / kStageChunk;
   const uint64_t want = (max_chunks + kExpandWarps - 1) / kExpandWarps;
-  const uint64_t lim = (uint64_t)num_sms * 2;  // 2 CTAs of 4 warps per SM (shared memory)
+  const uint64_t lim = (uint64_t)num_sms * 2;  // 2 CTAs of 8 warps per SM (shared memory)
   const int grid = (int)(want < lim ? want : lim);
   stage_expand_kernel<<<grid, kExpandWarps * 32, smem, st>>>(stage, stage_used, stage_cap16, wc, tile_offsets, pos,
                                                              cap);
