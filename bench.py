@@ -53,6 +53,14 @@ def parse():
     return ap.parse_args()
 
 
+def traffic_per_pass(config: str):
+    path = os.path.join(ROOT, "profiles", f"traffic_{config.lower()}.json")
+    try:
+        return float(json.load(open(path))["traffic_per_pattern_pass"])
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         d = json.load(open(MEASURED_PEAKS))
@@ -466,9 +474,9 @@ def run_native(args):
         "roofline": {
             "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4),
-            # DRAM read+write bytes per pattern pass, from the committed ncu capture of this kernel
-            # (profiles/r1_summary.md §6: batch of 8 c2 m=16 patterns, 1922 MB / 8); null for other configs
-            "traffic": 240.3e6 if args.config.lower() == "c2" else None,
+            # DRAM read+write bytes per pattern pass, from the committed ncu --set full capture of
+            # this kernel (profiles/traffic_c2.json, written by tools/ncu_traffic.py); null elsewhere
+            "traffic": traffic_per_pass(args.config),
             "traffic_unit": "bytes per pattern pass (algorithmic n = %d)" % spec.n, "avg_launch_us": round(search_ms * 1e3 / P, 2),
             "kernel": "search_kernel (count)", "peak_kind": peak_kind,
             "algorithmic_bytes_per_launch": "n (text bytes of the launch's view)",

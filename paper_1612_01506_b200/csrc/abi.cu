@@ -138,6 +138,8 @@ struct Tunables {
   uint32_t max_stages = 8;      // ring depth cap per CTA
   double filter_max_f = 0;      // AUTO: override of the FILTER threshold on f(pi(1)) (0 = built-in)
   bool auto_packed = true;      // AUTO may pick PACKED for small text alphabets
+  bool alternate = true;        // batches: odd patterns scan the text backwards (L2 reuse at the seam)
+  uint32_t l2_policy = 0;       // TMA load L2 policy: 0 evict_first, 1 evict_normal, 2 evict_last
 };
 
 const Tunables& tunables() {
@@ -148,6 +150,8 @@ const Tunables& tunables() {
     if (const char* e = std::getenv("SMGPU_STAGES")) x.max_stages = (uint32_t)std::atoi(e);
     if (const char* e = std::getenv("SMGPU_FILTER_MAX_F")) x.filter_max_f = std::atof(e);
     if (const char* e = std::getenv("SMGPU_AUTO_PACKED")) x.auto_packed = std::atoi(e) != 0;
+    if (const char* e = std::getenv("SMGPU_ALTERNATE")) x.alternate = std::atoi(e) != 0;
+    if (const char* e = std::getenv("SMGPU_L2_POLICY")) x.l2_policy = (uint32_t)std::atoi(e) % 3u;
     if (x.tile != 4096 && x.tile != 8192 && x.tile != 16384 && x.tile != 32768) x.tile = 32768;
     if (x.ctas_per_sm < 1 || x.ctas_per_sm > 3) x.ctas_per_sm = 2;
     if (x.max_stages < 2 || x.max_stages > (uint32_t)kMaxStages) x.max_stages = kMaxStages;
@@ -335,6 +339,7 @@ void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_
   L.a.npat = (uint32_t)ps.size();
   L.a.tbl_words = (uint32_t)L.e.size();
   L.a.ctr = counters_ptr();
+  L.a.l2_policy = tunables().l2_policy;
   // reporting launches reserve the per-warp position lists
   L.a.list_off = (kTblOff + 127) & ~127u;
   const uint32_t list_bytes = epilogue == kEpiCount ? 0u : (uint32_t)(kConsumerWarps * kListCap * 2);
@@ -354,6 +359,9 @@ void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_
       work += L.d[i].ntiles;
       L.d[i].work_end = work;
       L.d[i].count_out = q.count_out;
+      // consecutive passes over the same text alternate direction, so each pass starts on
+      // the tiles the previous one read last (still in the 126 MB L2); never changes results
+      L.d[i].reverse = tunables().alternate ? (uint32_t)(i & 1) : 0u;
       max_stage = std::max(max_stage, L.d[i].stage_len);
     }
     L.a.total_work = work;

@@ -72,7 +72,7 @@ struct PatDesc {
   uint32_t pre;        // buffer bytes before the tile (multiple of 16)
   uint32_t stage_len;  // bytes the tile's buffer holds = T + pre + post (multiple of 16)
   uint32_t tbl;        // index of this pattern's first entry in LaunchParams::e
-  uint32_t pad_;
+  uint32_t reverse;     // 1: tiles visited in descending order (alternating passes share the L2-resident seam)
 };
 
 struct LaunchArgs {
@@ -87,6 +87,7 @@ struct LaunchArgs {
   uint32_t npat;             // patterns in the batch
   uint32_t tbl_words;        // table entries
   uint32_t code_shift;       // PACKED: code(x) = (x >> code_shift) & (2^b - 1), injective on the text's symbols
+  uint32_t l2_policy;        // TMA loads: 0 evict_first, 1 evict_normal, 2 evict_last (performance only)
   uint32_t pack_off;         // PACKED: smem byte offset of the double-buffered code array
   uint32_t pack_bytes;       // PACKED: bytes of one code buffer
   uint32_t list_off;         // reporting: smem byte offset of the per-warp position lists [W][kListCap] u16

@@ -154,6 +154,7 @@ struct WorkIter {
       while (next >= P.d[k].work_end) ++k;
       kk = k;
       ti = next - (P.d[k].work_end - P.d[k].ntiles);
+      if (P.d[k].reverse) ti = P.d[k].ntiles - 1 - ti;  // alternating scan direction
     }
     next += gridDim.x;
     return true;
@@ -168,7 +169,8 @@ struct WorkIter {
 template <int EPI, int CAP>
 __device__ void produce(const LaunchParams<CAP>& P, uint8_t* ring, uint64_t* full, uint64_t* empty) {
   const LaunchArgs& a = P.a;
-  const uint64_t pol = l2_policy_evict_first();
+  const uint64_t pol = a.l2_policy == 2 ? l2_policy_evict_last()
+                       : a.l2_policy == 1 ? l2_policy_evict_normal() : l2_policy_evict_first();
   const int64_t tlo = (int64_t)a.delta, thi = (int64_t)(a.delta + a.n);
   uint32_t s = 0, ph = 0;  // stage and its use parity
   bool wrapped = false;

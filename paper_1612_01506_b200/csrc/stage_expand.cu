@@ -51,6 +51,14 @@ __device__ __forceinline__ void write_record(const uint8_t* rec, uint64_t out, u
   for (uint32_t r0 = 0; r0 < words && o < cap; r0 += 32) {
     const uint32_t i = r0 + lane;
     uint32_t mk = i < words ? bm[i] : 0u;
+    if (r0 + 32 <= words && __all_sync(0xFFFFFFFFu, mk == 0xFFFFFFFFu)) {
+      // every alignment of the round matches: positions are consecutive
+      const int64_t b0 = pos_base + (int64_t)(w * wspan + 32u * r0);
+      for (uint32_t q = lane; q < 1024u; q += 32)
+        if (o + q < cap) pos[o + q] = (uint64_t)(b0 + (int64_t)q);
+      o += 1024u;
+      continue;
+    }
     const uint32_t pc = __popc(mk);
     const uint32_t incl = warp_incl_scan_x(pc, lane);
     const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
