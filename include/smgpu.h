@@ -77,12 +77,17 @@ typedef enum sm_status {
  *     on the symbols present in t (from hist: it MUST be t's histogram); needs
  *     <= 4 text symbols and every pattern symbol present in t, else SM_EINVAL.
  *     For DNA / binary text (compare-bound regime).
+ *  SM_STRATEGY_PAIR: FILTER with the rarest-two-symbol chunk test: a 16-byte
+ *     chunk is queued only if one of its alignments matches pi(1) AND pi(2)
+ *     (m >= 2; m = 1 runs FILTER).  Best when pi(1) is too frequent for
+ *     FILTER's single-symbol chunk test to skip much.
  *  SM_STRATEGY_AUTO: chosen on the host from the text histogram. */
 typedef enum sm_strategy {
   SM_STRATEGY_AUTO = 0,
   SM_STRATEGY_FILTER = 1,
   SM_STRATEGY_BLOCK = 2,
-  SM_STRATEGY_PACKED = 3
+  SM_STRATEGY_PACKED = 3,
+  SM_STRATEGY_PAIR = 4
 } sm_strategy;
 
 #define SM_COUNT_ERROR UINT64_MAX

@@ -136,9 +136,10 @@ struct Tunables {
   uint32_t tile = 32768;        // text bytes per tile for large texts (4096 * CPL)
   int ctas_per_sm = 2;          // persistent CTAs per SM
   uint32_t max_stages = 8;      // ring depth cap per CTA
-  double filter_max_f = 0;      // AUTO: override of the FILTER threshold on f(pi(1)) (0 = built-in)
   bool auto_packed = true;      // AUTO may pick PACKED for small text alphabets
   bool alternate = true;        // batches: odd patterns scan the text backwards (L2 reuse at the seam)
+  double pair_min_hit = 0.12;   // AUTO: PAIR instead of FILTER when p[pi(1)] is in > this share of 16-B chunks
+  double block_min_hit = 0.3;   // AUTO: BLOCK / PACKED when a pi(1)&pi(2) survivor is in > this share
   uint32_t l2_policy = 0;       // TMA load L2 policy: 0 evict_first, 1 evict_normal, 2 evict_last
 };
 
@@ -148,12 +149,13 @@ const Tunables& tunables() {
     if (const char* e = std::getenv("SMGPU_TILE")) x.tile = (uint32_t)std::atoi(e);
     if (const char* e = std::getenv("SMGPU_CTAS_PER_SM")) x.ctas_per_sm = std::atoi(e);
     if (const char* e = std::getenv("SMGPU_STAGES")) x.max_stages = (uint32_t)std::atoi(e);
-    if (const char* e = std::getenv("SMGPU_FILTER_MAX_F")) x.filter_max_f = std::atof(e);
     if (const char* e = std::getenv("SMGPU_AUTO_PACKED")) x.auto_packed = std::atoi(e) != 0;
     if (const char* e = std::getenv("SMGPU_ALTERNATE")) x.alternate = std::atoi(e) != 0;
+    if (const char* e = std::getenv("SMGPU_PAIR_MIN_HIT")) x.pair_min_hit = std::atof(e);
+    if (const char* e = std::getenv("SMGPU_BLOCK_MIN_HIT")) x.block_min_hit = std::atof(e);
     if (const char* e = std::getenv("SMGPU_L2_POLICY")) x.l2_policy = (uint32_t)std::atoi(e) % 3u;
     if (x.tile != 4096 && x.tile != 8192 && x.tile != 16384 && x.tile != 32768) x.tile = 32768;
-    if (x.ctas_per_sm < 1 || x.ctas_per_sm > 3) x.ctas_per_sm = 2;
+    if (x.ctas_per_sm < 1 || x.ctas_per_sm > 4) x.ctas_per_sm = 2;
     if (x.max_stages < 2 || x.max_stages > (uint32_t)kMaxStages) x.max_stages = kMaxStages;
     return x;
   }();
@@ -208,7 +210,7 @@ int packed_projection(const uint64_t* hist, const uint8_t* p, size_t m, uint32_t
 
 sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist, const uint32_t* order,
                     uint32_t peel, int strategy, Plan& pl) {
-  if (strategy < SM_STRATEGY_AUTO || strategy > SM_STRATEGY_PACKED) return fail(SM_EINVAL, "bad strategy");
+  if (strategy < SM_STRATEGY_AUTO || strategy > SM_STRATEGY_PAIR) return fail(SM_EINVAL, "bad strategy");
   pl.order.resize(m);
   if (order) {
     if (!valid_permutation(order, m)) return fail(SM_EINVAL, "order is not a permutation of 0..m-1");
@@ -221,17 +223,26 @@ sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist
   for (int c = 0; c < 256; ++c) total += (double)hist[c];
   auto freq = [&](size_t k) { return total > 0 ? (double)hist[p[pl.order[k]]] / total : 0.0; };
   if (strategy == SM_STRATEGY_AUTO) {
-    // FILTER's cost grows with the share of 16-byte chunks holding p[pi(1)]; BLOCK's
-    // with the number of packed-byte steps.  Crossovers measured on B200
-    // (tools/strat_cmp.py, profiles/strategy_r1.md): m <= 2 -> BLOCK above f1 ~ 3.5%;
-    // m >= 3 -> BLOCK above f1 ~ 6%.
-    const double f1 = freq(0);
-    const double thr = tunables().filter_max_f > 0 ? tunables().filter_max_f : (m <= 2 ? 0.035 : 0.06);
-    strategy = f1 <= thr ? kFilter : kBlock;
-    if (strategy == kBlock && tunables().auto_packed) {  // small text alphabet: compare b-bit codes
-      const int pk = packed_projection(hist, p, m, &pl.code_shift);
-      if (pk) strategy = pk;
+    // Chunk-test hit rates (i.i.d. estimate from the histogram): FILTER queues the 16-byte
+    // chunks holding p[pi(1)] (h1), PAIR those with a pi(1)&pi(2) survivor (h12); each
+    // queued chunk costs a gather + two exact compares.  BLOCK (Alg. 4 over warp-blocks)
+    // has a flat cost and wins only when even the pair test passes most chunks.
+    // Crossovers measured on B200 (tools/pair_sweep.sh, profiles/strategy_r1.md).
+    const double f1 = freq(0), f12 = m >= 2 ? f1 * freq(1) : f1;
+    const double h1 = 1.0 - std::pow(1.0 - f1, 16.0), h12 = 1.0 - std::pow(1.0 - f12, 16.0);
+    if (h12 > tunables().block_min_hit) {
+      strategy = kBlock;
+      if (tunables().auto_packed) {  // small text alphabet: compare b-bit codes
+        const int pk = packed_projection(hist, p, m, &pl.code_shift);
+        if (pk) strategy = pk;
+      }
+    } else if (m >= 2 && h1 > tunables().pair_min_hit) {
+      strategy = kPair;
+    } else {
+      strategy = kFilter;
     }
+  } else if (strategy == SM_STRATEGY_PAIR) {
+    strategy = m >= 2 ? kPair : kFilter;
   } else if (strategy == SM_STRATEGY_PACKED) {
     strategy = packed_projection(hist, p, m, &pl.code_shift);
     if (!strategy)
@@ -250,6 +261,7 @@ sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist
   }
   pl.r = std::min<uint32_t>(peel, (uint32_t)m);
   if (pl.strategy == kFilter) pl.r = 1;
+  if (pl.strategy == kPair) pl.r = 2;  // pi(1), pi(2) tested together
   return SM_OK;
 }
 
@@ -276,7 +288,7 @@ void fill_desc(const Plan& pl, const uint8_t* p, size_t m, uint64_t delta, uint6
   d.r = pl.r;
   d.tbl = tbl_index;
   d.A = std::min<uint64_t>(n - m + 1, lim);
-  if (pl.strategy == kFilter) {
+  if (pl.strategy == kFilter || pl.strategy == kPair) {  // geometry of the pi(1)-bytes
     const uint32_t a1 = pl.order[0];
     d.a1 = a1;
     d.bc1 = (uint32_t)p[a1] * 0x01010101u;
@@ -300,7 +312,7 @@ void fill_desc(const Plan& pl, const uint8_t* p, size_t m, uint64_t delta, uint6
     d.ntiles = (delta + d.A - 1) / T + 1;
   }
   // edge tiles: only these need range masks (tile ti covers alignments x_base + [0, T))
-  const uint64_t shift = pl.strategy == kFilter ? d.a1 : 0;
+  const uint64_t shift = (pl.strategy == kFilter || pl.strategy == kPair) ? d.a1 : 0;
   const uint64_t first_full = (delta + shift + T - 1) / T;  // smallest k with k*T - shift >= delta
   d.edge_lo = first_full > d.k_begin ? first_full - d.k_begin : 0;
   const uint64_t kh = (delta + d.A + shift) / T;             // smallest k with (k+1)*T - shift > delta + A
@@ -440,7 +452,7 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
   // plan and launch as we go: a batch is launched as soon as it is full, so the GPU
   // starts on the first patterns while the host still orders the later ones
   std::vector<Planned> plans(P);
-  constexpr int kStrategies = 5;                  // index = strategy value (1..4)
+  constexpr int kStrategies = 6;                  // index = strategy value (1..5)
   std::vector<const Planned*> batch[kStrategies];
   size_t words[kStrategies] = {0, 0, 0, 0, 0};
   auto flush = [&](int strat) -> sm_status {
@@ -540,7 +552,7 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
   // a fixed slot range [item_base, item_base + ntiles) of the per-tile arrays in the
   // caller's order, so one scan gives the concatenated, pattern-ordered output layout
   std::vector<HostLaunch> Ls;
-  for (int strat : {(int)kFilter, (int)kBlock, (int)kPacked1, (int)kPacked2}) {
+  for (int strat : {(int)kFilter, (int)kPair, (int)kBlock, (int)kPacked1, (int)kPacked2}) {
     std::vector<const Planned*> run;
     size_t words = 0;
     auto flush = [&]() {
@@ -755,7 +767,7 @@ sm_status sm_count_batch(const uint8_t* const* p, const size_t* m, size_t P, con
                          void* stream) {
   if (P == 0) return SM_OK;
   if (!p || !m || !d_counts) return fail(SM_EINVAL, "NULL argument");
-  if (strategy < SM_STRATEGY_AUTO || strategy > SM_STRATEGY_PACKED) return fail(SM_EINVAL, "bad strategy");
+  if (strategy < SM_STRATEGY_AUTO || strategy > SM_STRATEGY_PAIR) return fail(SM_EINVAL, "bad strategy");
   for (size_t i = 0; i < P; ++i) {
     if (m[i] == 0) return fail(SM_EINVAL, "m[i] == 0: empty pattern is undefined (reading R2)");
     if (m[i] > SM_MAX_PATTERN) return fail(SM_EINVAL, "m[i] > SM_MAX_PATTERN (4096)");
@@ -776,7 +788,7 @@ sm_status sm_report_batch(const uint8_t* const* p, const size_t* m, size_t P, co
                           uint64_t* d_counts, uint64_t position_offset, void* stream) {
   if (P == 0) return SM_OK;
   if (!p || !m || !d_counts) return fail(SM_EINVAL, "NULL argument");
-  if (strategy < SM_STRATEGY_AUTO || strategy > SM_STRATEGY_PACKED) return fail(SM_EINVAL, "bad strategy");
+  if (strategy < SM_STRATEGY_AUTO || strategy > SM_STRATEGY_PAIR) return fail(SM_EINVAL, "bad strategy");
   for (size_t i = 0; i < P; ++i) {
     if (m[i] == 0) return fail(SM_EINVAL, "m[i] == 0: empty pattern is undefined (reading R2)");
     if (m[i] > SM_MAX_PATTERN) return fail(SM_EINVAL, "m[i] > SM_MAX_PATTERN (4096)");

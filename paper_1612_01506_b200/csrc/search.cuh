@@ -24,7 +24,8 @@ constexpr uint32_t kWarpTotOff = 2 * kMaxStages * 8;
 constexpr uint32_t kQueueOff = kWarpTotOff + 2 * kConsumerWarps * 4;
 constexpr uint32_t kTblOff = kQueueOff + kConsumerWarps * kQueueLen * 2;  // end of the fixed region
 
-enum Strategy : int { kFilter = 1, kBlock = 2, kPacked1 = 3, kPacked2 = 4 };  // kPackedB: b-bit codes
+// kPackedB: b-bit codes; kPair: FILTER whose chunk test covers pi(1) and pi(2) together
+enum Strategy : int { kFilter = 1, kBlock = 2, kPacked1 = 3, kPacked2 = 4, kPair = 5 };
 // kEpiCount: per-pattern counts.  kEpiStage: reporting pass 1 -- per-(pattern, tile) counts
 // plus the tile's matches staged compactly in global memory (per-warp u16 offset lists
 // or bitmaps), expanded into positions by stage_expand_kernel after the scan: the

@@ -15,6 +15,8 @@
 //   * FILTER: pi(1) (the rarest symbol) is tested over 16-byte
 //     chunks; flagged chunks are ballot-compacted, then pi(1), pi(2) compared
 //     exactly (peeling r = 2) and pi(3..m) verified per survivor with early exit.
+//   * PAIR: FILTER whose chunk test covers pi(1) AND pi(2) (one zero-byte test on the
+//     OR of the two XORs) -- the rarest-two-symbol filter, for frequent pi(1).
 //   * BLOCK: Alg. 4 as written: r peeled compares without a test,
 //     then the pi-ordered loop with a warp-uniform exit test (__any_sync).
 //   * PACKED: BLOCK on 1- or 2-bit codes of the text bytes (small alphabets).
@@ -219,6 +221,22 @@ __device__ __forceinline__ bool chunk_hit(const uint4 v, uint32_t bc) {
           0x80808080u) != 0;
 }
 
+// PAIR phase A: does some alignment of chunk c match BOTH pi(1) and pi(2)?  The byte
+// (t[x + pi(1)] ^ p[pi(1)]) | (t[x + pi(2)] ^ p[pi(2)]) is zero iff alignment x matches
+// both, so one borrow-based zero-byte test on the OR covers the two comparisons
+// (exact as a whole-chunk predicate, like chunk_hit).  QA = word offset of pi(2)'s window.
+template <int QA>
+__device__ __forceinline__ bool pair_hit(const uint8_t* buf, uint32_t c, uint32_t pre, uint32_t s2, uint32_t bc1,
+                                         uint32_t bc2) {
+  const uint4 v1 = lds128(buf + pre + 16u * c);
+  const uint4 v2 = window16_q<QA>(buf + 16u * c + (s2 & ~15u), (s2 & 3u) * 8u);
+  const uint32_t y0 = (v1.x ^ bc1) | (v2.x ^ bc2), y1 = (v1.y ^ bc1) | (v2.y ^ bc2);
+  const uint32_t y2 = (v1.z ^ bc1) | (v2.z ^ bc2), y3 = (v1.w ^ bc1) | (v2.w ^ bc2);
+  return ((((y0 - 0x01010101u) & ~y0) | ((y1 - 0x01010101u) & ~y1) | ((y2 - 0x01010101u) & ~y2) |
+           ((y3 - 0x01010101u) & ~y3)) &
+          0x80808080u) != 0;
+}
+
 // 0x80-per-byte flag words -> one word, bit (8k + 7 - i) <-> alignment 4i + k
 __device__ __forceinline__ uint32_t compress_found(const Found4& F) {
   return (F.f0 & 0x80808080u) | ((F.f1 & 0x80808080u) >> 1) | ((F.f2 & 0x80808080u) >> 2) |
@@ -388,9 +406,11 @@ __device__ __forceinline__ void filter_drain(const Pat& pt, const uint8_t* buf, 
 // One warp's share of a FILTER tile, in groups of kGroup chunk-rows: phase A
 // ballot-compacts the chunks whose pi(1)-bytes contain p[pi(1)] into the warp's
 // queue (ascending chunk order); phase B (filter_drain) verifies them.
-template <int CPL, class Sink>
-__device__ __forceinline__ void filter_tile(const Pat& pt, const uint8_t* buf, uint32_t cw0, int lane, uint16_t* qc,
-                                            bool edge, int32_t rlo, int32_t rhi, Sink& sink, Ctr& C) {
+// PA (PAIR strategy): phase A tests pi(1) and pi(2) together (pair_hit, pi(2)'s window
+// class QA), so only chunks with a pi(1)&pi(2) survivor are queued -- for frequent pi(1).
+template <int CPL, bool PA, int QA, class Sink>
+__device__ __forceinline__ void filter_tile_q(const Pat& pt, const uint8_t* buf, uint32_t cw0, int lane, uint16_t* qc,
+                                              bool edge, int32_t rlo, int32_t rhi, Sink& sink, Ctr& C) {
   C.add(kCtrChunks, 32u * CPL);
   constexpr int G = CPL < kGroup ? CPL : kGroup;
 #pragma unroll
@@ -400,7 +420,9 @@ __device__ __forceinline__ void filter_tile(const Pat& pt, const uint8_t* buf, u
     for (int it = g0; it < g0 + G; ++it) {
       const uint32_t c = cw0 + it * 32u + lane;
       SMGPU_DCHECK(pt.pre + 16u * c + 16u <= pt.lim);
-      const bool hit = chunk_hit(lds128(buf + pt.pre + 16u * c), pt.bc1);
+      bool hit;
+      if constexpr (PA) hit = pair_hit<QA>(buf, c, pt.pre, pt.s2, pt.bc1, pt.bc2);
+      else hit = chunk_hit(lds128(buf + pt.pre + 16u * c), pt.bc1);
       const uint32_t bal = __ballot_sync(0xFFFFFFFFu, hit);
       if (hit) qc[qlen + __popc(bal & lanemask_lt())] = (uint16_t)c;
       qlen += __popc(bal);
@@ -414,6 +436,23 @@ __device__ __forceinline__ void filter_tile(const Pat& pt, const uint8_t* buf, u
       default: filter_drain<3>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink, C); break;
     }
     __syncwarp();
+  }
+}
+
+template <int CPL, class Sink>
+__device__ __forceinline__ void filter_tile(const Pat& pt, const uint8_t* buf, uint32_t cw0, int lane, uint16_t* qc,
+                                            bool edge, int32_t rlo, int32_t rhi, Sink& sink, Ctr& C) {
+  filter_tile_q<CPL, false, 0>(pt, buf, cw0, lane, qc, edge, rlo, rhi, sink, C);
+}
+
+template <int CPL, class Sink>
+__device__ __forceinline__ void pair_tile(const Pat& pt, const uint8_t* buf, uint32_t cw0, int lane, uint16_t* qc,
+                                          bool edge, int32_t rlo, int32_t rhi, Sink& sink, Ctr& C) {
+  switch ((pt.s2 >> 2) & 3u) {  // warp-uniform
+    case 0: filter_tile_q<CPL, true, 0>(pt, buf, cw0, lane, qc, edge, rlo, rhi, sink, C); break;
+    case 1: filter_tile_q<CPL, true, 1>(pt, buf, cw0, lane, qc, edge, rlo, rhi, sink, C); break;
+    case 2: filter_tile_q<CPL, true, 2>(pt, buf, cw0, lane, qc, edge, rlo, rhi, sink, C); break;
+    default: filter_tile_q<CPL, true, 3>(pt, buf, cw0, lane, qc, edge, rlo, rhi, sink, C); break;
   }
 }
 
@@ -878,7 +917,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
   uint32_t acc = 0;  // kEpiCount: this lane's matches of pattern kc so far
   Ctr C;
 #ifdef SMGPU_COUNTERS
-  C.v[kCtrAlphaEff] = (STRAT == kFilter) ? 0ull : 512ull * CPL;
+  C.v[kCtrAlphaEff] = (STRAT == kFilter || STRAT == kPair) ? 0ull : 512ull * CPL;
 #endif
   WorkIter<EPI, CAP> items(P);
   uint32_t k;
@@ -897,7 +936,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
     const uint8_t* buf = ring + (size_t)s * a.stage_stride;
     const Pat pt{d.m, d.r, d.a1, d.bc1, d.s2, d.bc2, d.pre, d.stage_len, P.e + d.tbl};
     const bool edge = ti < d.edge_lo || ti >= d.edge_hi;  // tile holds invalid alignments
-    const int64_t shift = (STRAT == kFilter) ? (int64_t)d.a1 : 0;
+    const int64_t shift = (STRAT == kFilter || STRAT == kPair) ? (int64_t)d.a1 : 0;
     const int64_t x_base = (int64_t)((d.k_begin + ti) * T) - shift;  // alignment offset of u = 0
     const int64_t pos_base = x_base - (int64_t)a.delta + (int64_t)a.pos_offset;  // position of u = 0
     int32_t rlo = 0, rhi = (int32_t)T;
@@ -908,14 +947,18 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
     }
     bool released = false;  // the stage's bytes were handed back to the producer
 
-    if (STRAT == kFilter) {
+    if (STRAT == kFilter || STRAT == kPair) {
+      auto ftile = [&](auto& sink, Ctr& cc) {
+        if constexpr (STRAT == kPair) pair_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, sink, cc);
+        else filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, sink, cc);
+      };
       if (EPI == kEpiCount) {
         CountSink cs;
-        filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, cs, C);
+        ftile(cs, C);
         acc += cs.n;
       } else if (EPI == kEpiStage) {
         StageSink sk{list, cw0};
-        filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, sk, C);
+        ftile(sk, C);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         released = true;
@@ -923,7 +966,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
         if (wcnt) stage_warp<CPL, true>(a, d, list, salloc, warp, lane, item, pos_base, wcnt);
       } else {  // overflow pass: buffer this warp's matches, exchange warp totals, write coalesced
         AppendSink<true> as{list};
-        filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, as, C);
+        ftile(as, C);
         uint64_t run = publish_and_offset(a, s_wt, par, warp, lane, item, as.n);
         if (as.n <= (uint32_t)kListCap) {
           write_list(a, list, as.n, run, pos_base, lane);
@@ -931,7 +974,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
           WriteSink<> ws{run, pos_base, a.pos, a.cap};
           {
             Ctr C2;  // a recomputation: not counted again
-            filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, ws, C2);
+            ftile(ws, C2);
           }
         }
         par ^= 1u;

@@ -53,14 +53,16 @@ for n in ((1 << 20) + 333, (16 << 20) + 77):
                     print(("ok " if ok else "MISMATCH ") + f"n={n} sigma={syms.size} m={m} strat={strategy} r={peel} "
                           f"alpha={c['alpha_eff']} steps={c['steps']}/{steps} blocks={c['blocks']}/{blocks} "
                           f"count={got}/{want}")
-            if m >= 2:  # FILTER: survivors of the two peeled comparisons pi(1), pi(2)
-                got, c = run(p, a, t, sm.SM_STRATEGY_FILTER, order=pi.tolist())
+            for fs in (sm.SM_STRATEGY_FILTER, sm.SM_STRATEGY_PAIR):  # survivors of pi(1), pi(2)
+                if m < 2:
+                    break
+                got, c = run(p, a, t, fs, order=pi.tolist())
                 A = n - m + 1
                 a1, a2 = int(pi[0]), int(pi[1])
                 surv = int(np.count_nonzero((a[a1:a1 + A] == p[a1]) & (a[a2:a2 + A] == p[a2])))
                 ok = c["filter_survivors"] == surv and got == oracle.naive_count(p, a)
                 fails += not ok
-                print(("ok " if ok else "MISMATCH ") + f"FILTER n={n} sigma={syms.size} m={m} "
+                print(("ok " if ok else "MISMATCH ") + f"FILTER/PAIR({fs}) n={n} sigma={syms.size} m={m} "
                       f"survivors={c['filter_survivors']}/{surv} queued={c['filter_queued']} verify={c['filter_verify']}")
 print("counters workload done, mismatches:", fails)
 sys.exit(1 if fails else 0)

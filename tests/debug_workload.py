@@ -26,7 +26,7 @@ for alpha in (b"ACGT", b"\x00\x01", bytes(range(32, 127)), b"a"):
                 if m <= n:
                     s = int(rng.integers(0, n - m + 1))
                     pats.append(a[s:s + m].tobytes())
-            strategies = [1, 2] + ([3] if len(alpha) <= 4 else [])
+            strategies = [1, 2, 4] + ([3] if len(alpha) <= 4 else [])
             for strat in strategies:
                 d = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
                 sm.sm_count_batch(pats, t, d, hist=h, strategy=strat)

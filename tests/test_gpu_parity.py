@@ -59,7 +59,7 @@ def test_fig1(sm):
     pos, total = sm.sm_report(p, t)
     assert total == g["count"] and pos.cpu().tolist() == g["positions_0based"]
     assert sm.sm_symbol_order(t, p) == g["order_0based"]
-    for strat in (1, 2):
+    for strat in (1, 2, 4):
         for r in (1, 2, 3, 4):
             assert count_async(sm, p, t, strategy=strat, peel=r) == 1
 
@@ -69,7 +69,7 @@ def test_fig1(sm):
 def test_periodic_closed_form(sm, n):
     t = dev(np.full(n, 0x61, dtype=np.uint8), offset=n % 7)
     for m in (1, 2, 17, 1000):
-        for strat in (0, 1, 2):
+        for strat in (0, 1, 2, 4):
             want = max(n - m + 1, 0)
             assert count_async(sm, b"a" * m, t, strategy=strat) == want, (n, m, strat)
             assert count_async(sm, b"a" * (m - 1) + b"b", t, strategy=strat) == 0
@@ -150,7 +150,7 @@ def test_random_differential_count(sm):
         t = dev(a, off)
         want = oracle.naive_count(p, a)
         h = oracle.hist(a)
-        strat = int(rng.integers(0, 3))
+        strat = int(rng.choice([0, 1, 2, 4]))
         peel = int(rng.integers(0, m + 2))
         order = rng.permutation(m).tolist() if rng.random() < 0.4 else None
         got = count_async(sm, p, t, hist=h, order=order, peel=peel, strategy=strat)
@@ -164,7 +164,7 @@ def test_random_differential_report(sm):
         off = int(rng.integers(0, 16))
         t = dev(a, off)
         want = oracle.naive_report(p, a)
-        strat = int(rng.integers(0, 3))
+        strat = int(rng.choice([0, 1, 2, 4]))
         order = rng.permutation(len(p)).tolist() if rng.random() < 0.3 else None
         pos, total = report_async(sm, p, t, cap=want.size + 3, hist=oracle.hist(a), order=order, strategy=strat)
         assert total == want.size
@@ -175,7 +175,7 @@ def test_report_truncation(sm):
     a = np.frombuffer(b"ab" * 5000, dtype=np.uint8)
     t = dev(a)
     want = oracle.naive_report(b"ab", a)
-    for strat in (1, 2):
+    for strat in (1, 2, 4):
         pos, total = report_async(sm, b"ab", t, cap=100, strategy=strat)
         assert total == 5000 and pos.tolist() == want[:100].tolist()
     pos, total = sm.sm_report(b"ab", t, cap=7)
@@ -187,7 +187,7 @@ def test_report_truncation(sm):
 def test_dense_report_every_alignment(sm):
     n = 300_003
     t = dev(np.full(n, 7, dtype=np.uint8), 3)
-    for m, strat in ((1, 2), (3, 2), (3, 1)):
+    for m, strat in ((1, 2), (3, 2), (3, 1), (3, 4), (1, 4)):
         pos, total = report_async(sm, bytes([7]) * m, t, cap=n, strategy=strat)
         assert total == n - m + 1
         assert np.array_equal(pos, np.arange(n - m + 1))
@@ -219,7 +219,7 @@ def test_tile_seams(sm):
                 t = dev(b, off)
                 want = oracle.naive_count(p.tobytes(), b)
                 assert want >= len(kept)
-                for strat in (1, 2):
+                for strat in (1, 2, 4):
                     assert count_async(sm, p.tobytes(), t, strategy=strat) == want, (n, m, off, strat)
 
 
@@ -234,7 +234,7 @@ def test_boundary_residues(sm):
                 p = a[n - m:].tobytes()      # occurrence ending at t[n-1]
                 want = oracle.naive_count(p, a)
                 t = dev(a, dn % 3)
-                for strat in (1, 2):
+                for strat in (1, 2, 4):
                     assert count_async(sm, p, t, strategy=strat) == want
 
 
@@ -288,7 +288,7 @@ def test_count_batch_strategies_agree(sm):
     t = dev(a, 1)
     pats = [p.data for p in synth.patterns("c2", spec=spec, per_m=4)]
     want = [oracle.naive_count(p, a) for p in pats]
-    for strat in (0, 1, 2):
+    for strat in (0, 1, 2, 4):
         d = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
         sm.sm_count_batch(pats, t, d, strategy=strat)   # hist computed on the device
         assert d.cpu().tolist() == want, strat
@@ -414,7 +414,7 @@ def test_ten_thousand_random_cases_batched(sm):
         t = dev(a, int(rng.integers(0, 16)))
         h = oracle.hist(a)
         want = [oracle.naive_count(p, a) for p in pats]
-        strats = [0, 1, 2] + ([3] if np.unique(a).size <= 4 else [])
+        strats = [0, 1, 2, 4] + ([3] if np.unique(a).size <= 4 else [])
         for strat in strats:
             try:
                 d = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
