@@ -373,7 +373,7 @@ void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_
       L.d[i].count_out = q.count_out;
       // consecutive passes over the same text alternate direction, so each pass starts on
       // the tiles the previous one read last (still in the 126 MB L2); never changes results
-      L.d[i].reverse = tunables().alternate ? (uint32_t)(i & 1) : 0u;
+      L.d[i].flags = tunables().alternate ? (uint32_t)(i & 1) : 0u;
       max_stage = std::max(max_stage, L.d[i].stage_len);
     }
     L.a.total_work = work;
@@ -394,6 +394,20 @@ void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_
     if (stages < 2 && T > 4096) {  // only a single very long pattern can get here
       T /= 2;
       continue;
+    }
+    if (packed) {
+      // PACKED: all r peeled steps run, so move the ones whose code window
+      // is register-resident (off < 32 for 1-bit codes in 32-alignment units, else < 16)
+      // to the front (stable) and tell the kernel how many: two branch-free loops
+      const uint32_t lim = (cbits == 1 && L.cpl >= 2) ? 32u : 16u;
+      for (size_t i = 0; i < ps.size(); ++i) {
+        PatDesc& d = L.d[i];
+        uint32_t* e = L.e.data() + d.tbl;
+        std::stable_partition(e, e + d.r, [&](uint32_t x) { return (x & 0xFFFFu) < lim; });
+        uint32_t r1 = 0;
+        while (r1 < d.r && (e[r1] & 0xFFFFu) < lim) ++r1;
+        d.flags |= std::min<uint32_t>(r1, 255u) << 8;
+      }
     }
     L.a.stages = std::min<uint32_t>(stages, tunables().max_stages);
     L.smem = (size_t)L.a.ring_off + (size_t)L.a.stages * L.a.stage_stride;

@@ -73,7 +73,9 @@ struct PatDesc {
   uint32_t pre;        // buffer bytes before the tile (multiple of 16)
   uint32_t stage_len;  // bytes the tile's buffer holds = T + pre + post (multiple of 16)
   uint32_t tbl;        // index of this pattern's first entry in LaunchParams::e
-  uint32_t reverse;     // 1: tiles visited in descending order (alternating passes share the L2-resident seam)
+  uint32_t flags;       // bit 0: tiles visited in descending order (alternating passes share the L2-resident
+                       // seam); bits 8..15 (PACKED): r1 = the first r1 peeled steps read only the register
+                       // window (the host moves them to the front of the peeled steps, which all run)
 };
 
 struct LaunchArgs {

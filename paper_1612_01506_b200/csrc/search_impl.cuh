@@ -103,6 +103,7 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 // Per-tile view of one pattern of the batch (read from the kernel parameters).
 struct Pat {
   uint32_t m, r, a1, bc1, s2, bc2, pre;
+  uint32_t r1;          // PACKED: leading peeled steps whose window is register-resident
   uint32_t lim;         // bytes of the tile's stage buffer that hold this pattern's data (stage_len)
   const uint32_t* tbl;  // this pattern's table in the kernel parameters (m entries, pi order; constant cache)
 };
@@ -156,7 +157,7 @@ struct WorkIter {
       while (next >= P.d[k].work_end) ++k;
       kk = k;
       ti = next - (P.d[k].work_end - P.d[k].ntiles);
-      if (P.d[k].reverse) ti = P.d[k].ntiles - 1 - ti;  // alternating scan direction
+      if (P.d[k].flags & 1u) ti = P.d[k].ntiles - 1 - ti;  // alternating scan direction
     }
     next += gridDim.x;
     return true;
@@ -561,7 +562,9 @@ __device__ __forceinline__ uint32_t gather2(uint32_t x) {
 // b = 1, bit 2j for b = 2).  W0/W1 = the code words holding positions 16c.. (kept in
 // registers, so steps with off < 16 need no shared-memory load).  All branches
 // are warp-uniform and taken once per step.
-template <int CPL, int B>
+// MODE 0: branch on the window (warp-uniform); 1: register window known (off < 16);
+// 2: shared-memory window known (off >= 16).
+template <int CPL, int B, int MODE = 0>
 __device__ __forceinline__ void packed_step(uint32_t (&F)[CPL], const uint32_t (&W0)[CPL], const uint32_t (&W1)[CPL],
                                             const uint32_t* pk32, uint32_t qbase, int lane, uint32_t e,
                                             uint32_t pk_words) {
@@ -569,7 +572,7 @@ __device__ __forceinline__ void packed_step(uint32_t (&F)[CPL], const uint32_t (
   const uint32_t rep = B == 2 ? ccode * 0x55555555u : 0u - ccode;
   // bit offset of position 16c + off relative to the start of W0 (lane parity matters for b = 1)
   const uint32_t u = B == 2 ? 2u * off : 16u * (uint32_t)(lane & 1) + off;
-  if (off < 16u) {  // warp-uniform; then u < 32 on every lane
+  if (MODE == 1 || (MODE == 0 && off < 16u)) {  // warp-uniform; then u < 32 on every lane
 #pragma unroll
     for (int it = 0; it < CPL; ++it) {
       const uint32_t w = __funnelshift_r(W0[it], W1[it], u);
@@ -640,22 +643,29 @@ __device__ __forceinline__ int packed_tile(const Pat& pt, const uint8_t* buf, ui
       W0[it] = pk32[dc];
       W1[it] = pk32[dc + 1];
     }
-    auto step = [&](uint32_t e) {
+    auto step_reg = [&](uint32_t e) {  // the window lies in W0:W1 (off < 32)
       const uint32_t off = e & 0xFFFFu, rep = 0u - (e >> 16);
-      if (off < 32u) {  // warp-uniform: the window lies in W0:W1
 #pragma unroll
-        for (int it = 0; it < D; ++it) F[it] &= ~(__funnelshift_r(W0[it], W1[it], off) ^ rep);
-      } else {
-        const uint32_t* p = pk32 + dc0 + (off >> 5);
+      for (int it = 0; it < D; ++it) F[it] &= ~(__funnelshift_r(W0[it], W1[it], off) ^ rep);
+    };
+    auto step_mem = [&](uint32_t e) {  // off >= 32: two code words from shared memory
+      const uint32_t off = e & 0xFFFFu, rep = 0u - (e >> 16);
+      const uint32_t* p = pk32 + dc0 + (off >> 5);
 #pragma unroll
-        for (int it = 0; it < D; ++it) {
-          SMGPU_DCHECK((uint32_t)(p + it * 32 - pk32) + 1u < pk_words);
-          F[it] &= ~(__funnelshift_r(p[it * 32], p[it * 32 + 1], off & 31u) ^ rep);
-        }
+      for (int it = 0; it < D; ++it) {
+        SMGPU_DCHECK((uint32_t)(p + it * 32 - pk32) + 1u < pk_words);
+        F[it] &= ~(__funnelshift_r(p[it * 32], p[it * 32 + 1], off & 31u) ^ rep);
       }
     };
+    auto step = [&](uint32_t e) {
+      if ((e & 0xFFFFu) < 32u) step_reg(e);  // warp-uniform
+      else step_mem(e);
+    };
+    // peeled: all r run, so their order is free -- the host put the r1
+    // register-window steps first, leaving two branch-free loops
     uint32_t k = 0;
-    for (; k < pt.r; ++k) step(pt.tbl[k]);  // peeled
+    for (; k < pt.r1; ++k) step_reg(pt.tbl[k]);
+    for (; k < pt.r; ++k) step_mem(pt.tbl[k]);
     for (; k < pt.m; ++k) {                // ordered loop with exit test
       uint32_t any = 0;
 #pragma unroll
@@ -685,8 +695,9 @@ __device__ __forceinline__ int packed_tile(const Pat& pt, const uint8_t* buf, ui
     W0[it] = pk32[q];
     W1[it] = pk32[q + 1];
   }
-  uint32_t k = 0;
-  for (; k < pt.r; ++k) packed_step<CPL, B>(F, W0, W1, pk32, qbase, lane, pt.tbl[k], pk_words);  // peeled
+  uint32_t k = 0;  // peeled: register-window steps first (see above)
+  for (; k < pt.r1; ++k) packed_step<CPL, B, 1>(F, W0, W1, pk32, qbase, lane, pt.tbl[k], pk_words);
+  for (; k < pt.r; ++k) packed_step<CPL, B, 2>(F, W0, W1, pk32, qbase, lane, pt.tbl[k], pk_words);
   for (; k < pt.m; ++k) {  // ordered loop with exit test, warp-uniform
     uint32_t any = 0;
 #pragma unroll
@@ -934,7 +945,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
     const uint64_t item = d.item_base + ti;
     mbar_wait(&full[s], ph);
     const uint8_t* buf = ring + (size_t)s * a.stage_stride;
-    const Pat pt{d.m, d.r, d.a1, d.bc1, d.s2, d.bc2, d.pre, d.stage_len, P.e + d.tbl};
+    const Pat pt{d.m, d.r, d.a1, d.bc1, d.s2, d.bc2, d.pre, (d.flags >> 8) & 0xFFu, d.stage_len, P.e + d.tbl};
     const bool edge = ti < d.edge_lo || ti >= d.edge_hi;  // tile holds invalid alignments
     const int64_t shift = (STRAT == kFilter || STRAT == kPair) ? (int64_t)d.a1 : 0;
     const int64_t x_base = (int64_t)((d.k_begin + ti) * T) - shift;  // alignment offset of u = 0
