@@ -63,6 +63,33 @@ def test_plan_policy(sm):
     assert s == sm.SM_STRATEGY_FILTER
 
 
+def test_plan_auto_rule(sm):
+    """AUTO (abi.cu make_plan, profiles/strategy_pair_r1.md): h1 = 1-(1-f1)^16 is FILTER's chunk
+    queue rate, h12 = 1-(1-f1 f2)^16 PAIR's (h1 for m = 1); BLOCK/PACKED if h12 > 0.3, else PAIR
+    if m >= 2 and h1 > 0.12, else FILTER."""
+    h = np.zeros(256, dtype=np.uint64)
+    # 20 symbols 'A'..'T': two frequent (10 % each), the rest rare
+    for i, c in enumerate(range(65, 85)):
+        h[c] = 1000 if i < 2 else 444
+    rare, freq = b"T", b"A"
+    s, _ = sm.sm_plan(rare + freq * 3, h)          # f1 ~ 4.9 %: h1 ~ 0.55 > 0.12, h12 ~ 0.08 -> PAIR
+    assert s == 5 and sm.STRATEGY_NAMES[s] == "pair"
+    s, _ = sm.sm_plan(rare, h)                     # m = 1: h12 := h1 ~ 0.51 > 0.3 -> BLOCK
+    assert s == sm.SM_STRATEGY_BLOCK
+    h[ord("T")] = 10                               # a rare pi(1): h1 ~ 0.9 %: FILTER
+    s, _ = sm.sm_plan(b"T" + freq * 3, h)
+    assert s == sm.SM_STRATEGY_FILTER
+    hb = np.zeros(256, dtype=np.uint64)
+    for c in range(65, 70):                        # 5 equally frequent symbols: h12 = 1-(1-1/25)^16 ~ 0.48
+        hb[c] = 1000
+    s, _ = sm.sm_plan(b"ABCDE", hb)
+    assert s == sm.SM_STRATEGY_BLOCK               # 5 symbols: no 2-bit code -> BLOCK
+    s, _ = sm.sm_plan(b"ABCDE", hb, strategy=sm.SM_STRATEGY_PAIR)
+    assert s == 5                                  # forced
+    s, _ = sm.sm_plan(b"A", hb, strategy=sm.SM_STRATEGY_PAIR)
+    assert s == sm.SM_STRATEGY_FILTER              # PAIR needs pi(2): m = 1 runs FILTER
+
+
 def test_argument_errors_without_gpu(sm):
     lib = sm.load_library()
     host = (ctypes.c_uint8 * 8)()
