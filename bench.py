@@ -36,7 +36,7 @@ METRIC = "text GB/s scanned per pattern (device-timed) vs m; % of B200 HBM peak,
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["native", "reference"], default="native")
     ap.add_argument("--config", default="c2")
@@ -93,9 +93,13 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
-    def stop(self):
+    def mark(self):
+        """Host time of a region boundary (samples are kept only between mark() calls)."""
+        return time.time()
+
+    def stop(self, t0=None, t1=None):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -105,7 +109,8 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = [ln for t, ln in self.lines if (t0 is None or t >= t0) and (t1 is None or t <= t1 + 0.06)]
+        for ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 7:
                 continue
@@ -307,19 +312,22 @@ def run_native(args):
     # ---------------- timed region (device time, max over ranks)
     clk = ClockSampler(local)
     clk.start()
+    time.sleep(0.3)  # let nvidia-smi deliver its first sample before the timed region
     launches0 = sm.sm_launch_count()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
+    h0 = clk.mark()
     start.record(stream)
     for s in range(args.steps):
         step(evs[s])
     end.record(stream)
     barrier()
+    h1 = clk.mark()
     launches = sm.sm_launch_count() - launches0
     total_ms = start.elapsed_time(end)
     search_ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps   # the P search launches of a step
-    clocks = clk.stop()
+    clocks = clk.stop(h0, h1)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

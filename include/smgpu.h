@@ -152,6 +152,21 @@ sm_status sm_count_batch(const uint8_t* const* p, const size_t* m, size_t P, con
                          size_t max_alignments, const uint64_t* hist, int strategy, uint64_t* d_counts,
                          void* stream);
 
+/* Multi-GPU counting with the all-reduce fused into the kernel epilogue (NEXT-4):
+ * as sm_count_batch, but mc_counts (u64[P]) is the NVLink MULTICAST address of a
+ * buffer bound on every rank of the group (e.g. torch symmetric memory's
+ * multicast_ptr, or cuMulticastCreate + cuMulticastBindMem); each warp adds its
+ * popcount sum with one multimem.red (NVLS reduction in the switch), so when all
+ * ranks' launches have completed, every rank's own copy holds the sums over all
+ * ranks -- no separate collective.  The call does NOT zero the counts: every rank
+ * zeroes its copy and the group synchronises before any rank launches, and
+ * synchronises again (after its stream) before reading.  Same p, m, max_alignments
+ * (each rank passes its shard's owned alignments), hist and strategy as
+ * sm_count_batch.  SM_EINVAL for a misaligned mc_counts. */
+sm_status sm_count_batch_multicast(const uint8_t* const* p, const size_t* m, size_t P, const uint8_t* t, size_t n,
+                                   size_t max_alignments, const uint64_t* hist, int strategy, uint64_t* mc_counts,
+                                   void* stream);
+
 /* Enqueue the reporting version: the first min(count, cap) ascending
  * positions go to DEVICE pos[0..cap), the total count to DEVICE *d_count.
  * Truncation is detected by the caller (*d_count > cap) after the stream

@@ -41,7 +41,7 @@ STRATEGY_NAMES = {1: "filter", 2: "block", 3: "packed1", 4: "packed2", 5: "pair"
 
 EXPORTED_SYMBOLS = (
     "sm_count", "sm_report", "sm_symbol_order", "sm_histogram", "sm_order_from_histogram",
-    "sm_count_async", "sm_count_batch", "sm_report_async", "sm_report_batch", "sm_heuristic_order", "sm_plan", "sm_last_error", "sm_last_error_message",
+    "sm_count_async", "sm_count_batch", "sm_count_batch_multicast", "sm_report_async", "sm_report_batch", "sm_heuristic_order", "sm_plan", "sm_last_error", "sm_last_error_message",
     "sm_clear_error", "sm_status_string", "sm_version", "sm_launch_count", "sm_counters",
 )
 COUNTER_NAMES = ("warp_tiles", "blocks", "steps", "filter_chunks", "filter_queued", "filter_survivors",
@@ -86,6 +86,8 @@ def load_library(path: str = LIB_PATH):
     lib.sm_count_async.argtypes = [_u8p, _sz, _u8p, _sz, _vp, _vp, ctypes.c_uint32, ctypes.c_int, _vp, _vp]
     lib.sm_count_batch.restype = ctypes.c_int
     lib.sm_count_batch.argtypes = [_vp, _vp, _sz, _u8p, _sz, _sz, _vp, ctypes.c_int, _vp, _vp]
+    lib.sm_count_batch_multicast.restype = ctypes.c_int
+    lib.sm_count_batch_multicast.argtypes = [_vp, _vp, _sz, _u8p, _sz, _sz, _vp, ctypes.c_int, _vp, _vp]
     lib.sm_report_batch.restype = ctypes.c_int
     lib.sm_report_batch.argtypes = [_vp, _vp, _sz, _u8p, _sz, _sz, _vp, ctypes.c_int, _vp, _sz, _vp,
                                     ctypes.c_uint64, _vp]
@@ -285,6 +287,22 @@ def sm_count_batch(patterns, t, d_counts, hist=None, max_alignments: Optional[in
     dptr = d_counts if isinstance(d_counts, int) else d_counts.data_ptr()
     s = lib.sm_count_batch(ctypes.addressof(pb.ptrs), ctypes.addressof(pb.lens), pb.P, tp, n, lim, _np_ptr(h),
                            strategy, dptr, _stream(stream))
+    if s != SM_OK:
+        _raise(s)
+
+
+def sm_count_batch_multicast(patterns, t, mc_counts: int, hist=None, max_alignments: Optional[int] = None,
+                             strategy: int = SM_STRATEGY_AUTO, stream=None) -> None:
+    """NEXT-4: counts with the all-reduce fused into the kernel (multimem.red on the NVLink
+    multicast address mc_counts of a u64[P] buffer bound on every rank; see smgpu.h).
+    The caller zeroes its copy and synchronises the group before and after."""
+    lib = load_library()
+    pb = patterns if isinstance(patterns, PatternBatch) else PatternBatch(patterns)
+    tp, n = _text(t)
+    h = _u64_host(hist)
+    lim = (1 << 64) - 1 if max_alignments is None else int(max_alignments)
+    s = lib.sm_count_batch_multicast(ctypes.addressof(pb.ptrs), ctypes.addressof(pb.lens), pb.P, tp, n, lim,
+                                     _np_ptr(h), strategy, int(mc_counts), _stream(stream))
     if s != SM_OK:
         _raise(s)
 

@@ -453,9 +453,10 @@ sm_status enqueue_count(const uint8_t* p, size_t m, const uint8_t* t, size_t n, 
 // (each launch runs every one of its patterns as a full pass over the text).
 sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t P, const uint8_t* t, size_t n,
                               uint64_t lim, const uint64_t* hist, int strategy, uint64_t* d_counts,
-                              cudaStream_t st) {
+                              cudaStream_t st, bool multicast = false) {
   if (P == 0) return SM_OK;
-  SM_CUDA_TRY(cudaMemsetAsync(d_counts, 0, P * sizeof(uint64_t), st), "cudaMemsetAsync(counts)");
+  if (!multicast)  // multicast counts are zeroed by every rank on its own copy (see smgpu.h)
+    SM_CUDA_TRY(cudaMemsetAsync(d_counts, 0, P * sizeof(uint64_t), st), "cudaMemsetAsync(counts)");
   uint64_t hb[256];
   const uint64_t* h = hist;
   if (!h) {
@@ -473,6 +474,7 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
     if (batch[strat].empty()) return SM_OK;
     HostLaunch L;
     build_launch(batch[strat], t, n, lim, kEpiCount, L);
+    L.a.count_mc = multicast ? 1u : 0u;
     batch[strat].clear();
     words[strat] = 0;
     return launch_checked(L, st, "search kernel (batch)");
@@ -795,6 +797,27 @@ sm_status sm_count_batch(const uint8_t* const* p, const size_t* m, size_t P, con
   sm_status s = check_device_ptr(d_counts, "d_counts");
   if (s != SM_OK) return s;
   return enqueue_count_batch(p, m, P, t, n, (uint64_t)max_alignments, hist, strategy, d_counts, as_stream(stream));
+}
+
+sm_status sm_count_batch_multicast(const uint8_t* const* p, const size_t* m, size_t P, const uint8_t* t, size_t n,
+                                   size_t max_alignments, const uint64_t* hist, int strategy, uint64_t* mc_counts,
+                                   void* stream) {
+  if (P == 0) return SM_OK;
+  if (!p || !m || !mc_counts) return fail(SM_EINVAL, "NULL argument");
+  if (strategy < SM_STRATEGY_AUTO || strategy > SM_STRATEGY_PAIR) return fail(SM_EINVAL, "bad strategy");
+  for (size_t i = 0; i < P; ++i) {
+    if (m[i] == 0) return fail(SM_EINVAL, "m[i] == 0: empty pattern is undefined (reading R2)");
+    if (m[i] > SM_MAX_PATTERN) return fail(SM_EINVAL, "m[i] > SM_MAX_PATTERN (4096)");
+    if (!p[i]) return fail(SM_EINVAL, "p[i] is NULL");
+  }
+  if (n > 0) {
+    if (!t) return fail(SM_EINVAL, "t is NULL with n > 0");
+    sm_status s = check_device_ptr(t, "t");
+    if (s != SM_OK) return s;
+  }
+  if (reinterpret_cast<uintptr_t>(mc_counts) & 7u) return fail(SM_EINVAL, "mc_counts must be 8-byte aligned");
+  return enqueue_count_batch(p, m, P, t, n, (uint64_t)max_alignments, hist, strategy, mc_counts, as_stream(stream),
+                             true);
 }
 
 sm_status sm_report_batch(const uint8_t* const* p, const size_t* m, size_t P, const uint8_t* t, size_t n,

@@ -121,6 +121,14 @@ __device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gmem_src
 }
 
 // ---------------------------------------------------------------------------
+// NVLink SHARP (NVLS) reduction through a multicast address: the add is applied to the
+// bound buffer of every device in the multicast group (PTX multimem.red).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void multimem_red_add_u64(void* mc_addr, unsigned long long v) {
+  asm volatile("multimem.red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(mc_addr), "l"(v) : "memory");
+}
+
+// ---------------------------------------------------------------------------
 // global loads
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint8_t ldg_u8_nc(const uint8_t* p) {

@@ -100,6 +100,14 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return r;
 }
 
+// A6: add a warp's popcount sum to its pattern's count -- one u64
+// atomic, or, for a multi-GPU count (NEXT-4), one NVLS multimem reduction into every
+// rank's copy of the counts (the all-reduce fused into the epilogue).
+__device__ __forceinline__ void count_add(const LaunchArgs& a, uint64_t* out, uint32_t v) {
+  if (a.count_mc) multimem_red_add_u64(out, (unsigned long long)v);
+  else atomicAdd(reinterpret_cast<unsigned long long*>(out), (unsigned long long)v);
+}
+
 // Per-tile view of one pattern of the batch (read from the kernel parameters).
 struct Pat {
   uint32_t m, r, a1, bc1, s2, bc2, pre;
@@ -937,7 +945,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
     C.add(kCtrWarpTiles, 1);
     if (EPI == kEpiCount && k != kc) {  // flush pattern kc (warp-uniform; k only grows here)
       const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, acc);
-      if (lane == 0 && ws) atomicAdd(reinterpret_cast<unsigned long long*>(P.d[kc].count_out), (unsigned long long)ws);
+      if (lane == 0 && ws) count_add(a, P.d[kc].count_out, ws);
       acc = 0;
       kc = k;
     }
@@ -1057,7 +1065,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
 
   if (EPI == kEpiCount) {
     const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, acc);
-    if (lane == 0 && ws) atomicAdd(reinterpret_cast<unsigned long long*>(P.d[kc].count_out), (unsigned long long)ws);
+    if (lane == 0 && ws) count_add(a, P.d[kc].count_out, ws);
   }
   C.flush(a.ctr, lane);
 }

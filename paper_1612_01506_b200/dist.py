@@ -11,7 +11,10 @@ rank and the per-rank counts add up to the global count (no overlap, no gap).
 Exchanges (torch.distributed over NCCL / NVLink; gloo on CPU in the tests):
   * once per text: all_reduce(SUM) of the owned-byte histograms, so every rank
     derives the same rarest-first order pi as a 1-GPU run (reading R14);
-  * per pattern batch: all_reduce(SUM) of the device int64 counts.
+  * per pattern batch: all_reduce(SUM) of the device int64 counts -- or, where the
+    platform provides NVLink multicast (torch symmetric memory), no collective at
+    all: the count kernel reduces into every rank's copy with multimem.red
+    (count_sharded_fused, NEXT-4).
 """
 from __future__ import annotations
 
@@ -103,6 +106,51 @@ def count_sharded(patterns, shard_text, shard: Shard, hist, counts=None, group=N
     sm.sm_count_batch(pb, held, counts, hist=hist, max_alignments=shard.owned_bytes, strategy=strategy,
                       stream=stream)
     return allreduce_sum_(counts, group)
+
+
+class MulticastCounts:
+    """NEXT-4: an int64 count buffer in torch symmetric memory whose NVLink multicast
+    address the count kernel reduces into (sm_count_batch_multicast: multimem.red in the
+    epilogue, the all-reduce fused into the search).  `available` is False when the
+    platform gives no multicast pointer (e.g. a single-GPU box, where cuMulticastCreate is
+    refused); count_sharded_fused then uses count_sharded's NCCL all-reduce instead."""
+
+    def __init__(self, P: int, device, group=None):
+        import torch
+        import torch.distributed as dist
+        self.P, self.group, self.available = P, group, False
+        self.local = None
+        try:
+            import torch.distributed._symmetric_memory as symm_mem
+            self.local = symm_mem.empty(max(P, 1), dtype=torch.int64, device=device)
+            h = symm_mem.rendezvous(self.local, group if group is not None else dist.group.WORLD)
+            self.mc_ptr = int(getattr(h, "multicast_ptr", 0) or 0)
+            self.available = self.mc_ptr != 0
+        except Exception:
+            self.available = False
+
+
+def count_sharded_fused(patterns, shard_text, shard: Shard, hist, mc: "MulticastCounts", group=None,
+                        strategy: int = 0):
+    """Global counts with the reduction fused into the kernel when `mc.available`:
+    zero the local copy, barrier, one multicast count launch per batch, device sync,
+    barrier -> every rank's mc.local holds the global sums.  Else count_sharded."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1612_01506_b200 as sm
+    if not mc.available:
+        return count_sharded(patterns, shard_text, shard, hist, group=group, strategy=strategy)
+    pb = patterns if isinstance(patterns, sm.PatternBatch) else sm.PatternBatch(patterns)
+    shard.view_len(max((len(p) for p in pb.data), default=1))  # halo check
+    mc.local.zero_()
+    torch.cuda.synchronize()
+    dist.barrier(group=group)
+    sm.sm_count_batch_multicast(pb, shard_text[: shard.held_len], mc.mc_ptr, hist=hist,
+                                max_alignments=shard.owned_bytes, strategy=strategy)
+    torch.cuda.synchronize()
+    dist.barrier(group=group)
+    return mc.local[: pb.P]
 
 
 def gather_reports(local_counts, local_pos, group=None):
