@@ -152,13 +152,13 @@ sm_status sm_count_batch(const uint8_t* const* p, const size_t* m, size_t P, con
                          size_t max_alignments, const uint64_t* hist, int strategy, uint64_t* d_counts,
                          void* stream);
 
-/* Multi-GPU counting with the all-reduce fused into the kernel epilogue (NEXT-4):
- * as sm_count_batch, but mc_counts (u64[P]) is the NVLink MULTICAST address of a
- * buffer bound on every rank of the group (e.g. torch symmetric memory's
- * multicast_ptr, or cuMulticastCreate + cuMulticastBindMem); each warp adds its
- * popcount sum with one multimem.red (NVLS reduction in the switch), so when all
- * ranks' launches have completed, every rank's own copy holds the sums over all
- * ranks -- no separate collective.  The call does NOT zero the counts: every rank
+/* Multi-GPU counting without a collective call (NEXT-4): as sm_count_batch, but
+ * mc_counts (u64[P]) is the NVLink MULTICAST address of a buffer bound on every
+ * rank of the group (e.g. torch symmetric memory's multicast_ptr, or
+ * cuMulticastCreate + cuMulticastBindMem); after the search launches a small kernel
+ * adds this rank's counts with one multimem.red per pattern (NVLS reduction in the
+ * switch), so when all ranks' work has completed, every rank's own copy holds the
+ * sums over all ranks.  The call does NOT zero the counts: every rank
  * zeroes its copy and the group synchronises before any rank launches, and
  * synchronises again (after its stream) before reading.  Same p, m, max_alignments
  * (each rank passes its shard's owned alignments), hist and strategy as

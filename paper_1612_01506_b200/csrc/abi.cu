@@ -453,10 +453,9 @@ sm_status enqueue_count(const uint8_t* p, size_t m, const uint8_t* t, size_t n, 
 // (each launch runs every one of its patterns as a full pass over the text).
 sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t P, const uint8_t* t, size_t n,
                               uint64_t lim, const uint64_t* hist, int strategy, uint64_t* d_counts,
-                              cudaStream_t st, bool multicast = false) {
+                              cudaStream_t st) {
   if (P == 0) return SM_OK;
-  if (!multicast)  // multicast counts are zeroed by every rank on its own copy (see smgpu.h)
-    SM_CUDA_TRY(cudaMemsetAsync(d_counts, 0, P * sizeof(uint64_t), st), "cudaMemsetAsync(counts)");
+  SM_CUDA_TRY(cudaMemsetAsync(d_counts, 0, P * sizeof(uint64_t), st), "cudaMemsetAsync(counts)");
   uint64_t hb[256];
   const uint64_t* h = hist;
   if (!h) {
@@ -474,7 +473,6 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
     if (batch[strat].empty()) return SM_OK;
     HostLaunch L;
     build_launch(batch[strat], t, n, lim, kEpiCount, L);
-    L.a.count_mc = multicast ? 1u : 0u;
     batch[strat].clear();
     words[strat] = 0;
     return launch_checked(L, st, "search kernel (batch)");
@@ -816,8 +814,17 @@ sm_status sm_count_batch_multicast(const uint8_t* const* p, const size_t* m, siz
     if (s != SM_OK) return s;
   }
   if (reinterpret_cast<uintptr_t>(mc_counts) & 7u) return fail(SM_EINVAL, "mc_counts must be 8-byte aligned");
-  return enqueue_count_batch(p, m, P, t, n, (uint64_t)max_alignments, hist, strategy, mc_counts, as_stream(stream),
-                             true);
+  cudaStream_t st = as_stream(stream);
+  uint64_t* local = nullptr;  // this rank's counts, then one multimem.red per pattern
+  SM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&local), P * sizeof(uint64_t), st), "cudaMallocAsync(counts)");
+  sm_status s = enqueue_count_batch(p, m, P, t, n, (uint64_t)max_alignments, hist, strategy, local, st);
+  if (s == SM_OK) {
+    cudaError_t e = launch_nvls_add(local, mc_counts, P, st);
+    if (e == cudaSuccess) ++g_launches;
+    else s = cuda_fail(e, "nvls reduction");
+  }
+  cudaFreeAsync(local, st);
+  return s;
 }
 
 sm_status sm_report_batch(const uint8_t* const* p, const size_t* m, size_t P, const uint8_t* t, size_t n,

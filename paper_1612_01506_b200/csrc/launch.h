@@ -33,6 +33,9 @@ cudaError_t launch_stage_expand(const uint8_t* stage, const unsigned long long* 
                                 const uint16_t* wc, const uint64_t* tile_offsets, uint64_t* pos, uint64_t cap,
                                 int num_sms, cudaStream_t st);
 
+// NEXT-4: mc[i] += local[i] through an NVLink multicast address (multimem.red)
+cudaError_t launch_nvls_add(const uint64_t* local, uint64_t* mc, uint64_t P, cudaStream_t st);
+
 // exclusive prefix over items of the sum of wc[item][0..8) (u16 warp counts)
 cudaError_t exclusive_scan_wc(const uint16_t* wc, uint64_t* out, uint64_t items, void* temp, size_t* temp_bytes,
                               cudaStream_t st);

@@ -91,8 +91,6 @@ struct LaunchArgs {
   uint32_t tbl_words;        // table entries
   uint32_t code_shift;       // PACKED: code(x) = (x >> code_shift) & (2^b - 1), injective on the text's symbols
   uint32_t l2_policy;        // TMA loads: 0 evict_first, 1 evict_normal, 2 evict_last (performance only)
-  uint32_t count_mc;         // kEpiCount: count_out are NVLink multicast addresses (multimem.red: the
-                             // per-pattern sums land in every rank's copy, NEXT-4)
   uint32_t pack_off;         // PACKED: smem byte offset of the double-buffered code array
   uint32_t pack_bytes;       // PACKED: bytes of one code buffer
   uint32_t list_off;         // reporting: smem byte offset of the per-warp position lists [W][kListCap] u16

@@ -100,12 +100,12 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return r;
 }
 
-// A6: add a warp's popcount sum to its pattern's count -- one u64
-// atomic, or, for a multi-GPU count (NEXT-4), one NVLS multimem reduction into every
-// rank's copy of the counts (the all-reduce fused into the epilogue).
-__device__ __forceinline__ void count_add(const LaunchArgs& a, uint64_t* out, uint32_t v) {
-  if (a.count_mc) multimem_red_add_u64(out, (unsigned long long)v);
-  else atomicAdd(reinterpret_cast<unsigned long long*>(out), (unsigned long long)v);
+// A6: add a warp's popcount sum to its pattern's count (one u64 atomic).
+// (The NVLS multicast reduction of multi-GPU counts runs in its own small kernel: an
+// inline-asm multimem.red here is a convergent operation that made the compiler add
+// reconvergence barriers throughout this kernel, +7 % instructions.)
+__device__ __forceinline__ void count_add(const LaunchArgs&, uint64_t* out, uint32_t v) {
+  atomicAdd(reinterpret_cast<unsigned long long*>(out), (unsigned long long)v);
 }
 
 // Per-tile view of one pattern of the batch (read from the kernel parameters).
@@ -860,9 +860,9 @@ __device__ __forceinline__ void stage_warp(const LaunchArgs& a, const PatDesc& d
         mk[j] = bm[lane * CPL + j];
         pc += __popc((uint32_t)mk[j]);
       }
+      __syncwarp();  // every lane holds its masks: the list is built in place over the bitmap
       const uint32_t incl = warp_incl_scan(pc, lane);
       uint32_t idx = incl - pc;
-      uint16_t* L = reinterpret_cast<uint16_t*>(rec + kRecHeader);
       const uint32_t u0 = (uint32_t)warp * kWspan + 16u * (uint32_t)lane * CPL;
 #pragma unroll
       for (int j = 0; j < CPL; ++j) {
@@ -870,9 +870,13 @@ __device__ __forceinline__ void stage_warp(const LaunchArgs& a, const PatDesc& d
         while (m) {
           const uint32_t b = __ffs(m) - 1;
           m &= m - 1;
-          L[idx++] = (uint16_t)(u0 + 16u * j + b);
+          bm[idx++] = (uint16_t)(u0 + 16u * j + b);
         }
       }
+      __syncwarp();
+      const uint4* src = reinterpret_cast<const uint4*>(bm);  // coalesced 16-B copy of the list
+      uint4* dst = reinterpret_cast<uint4*>(rec + kRecHeader);
+      for (uint32_t i = lane; i < dbytes / 16u; i += 32) dst[i] = src[i];
     } else {  // dense: the bitmap (64 CPL bytes)
       const uint4* src = reinterpret_cast<const uint4*>(bm);
       uint4* dst = reinterpret_cast<uint4*>(rec + kRecHeader);

@@ -13,8 +13,8 @@ Exchanges (torch.distributed over NCCL / NVLink; gloo on CPU in the tests):
     derives the same rarest-first order pi as a 1-GPU run (reading R14);
   * per pattern batch: all_reduce(SUM) of the device int64 counts -- or, where the
     platform provides NVLink multicast (torch symmetric memory), no collective at
-    all: the count kernel reduces into every rank's copy with multimem.red
-    (count_sharded_fused, NEXT-4).
+    all: each rank's counts are added to every rank's copy with multimem.red through
+    an NVLink multicast address (count_sharded_fused, NEXT-4).
 """
 from __future__ import annotations
 
@@ -110,8 +110,8 @@ def count_sharded(patterns, shard_text, shard: Shard, hist, counts=None, group=N
 
 class MulticastCounts:
     """NEXT-4: an int64 count buffer in torch symmetric memory whose NVLink multicast
-    address the count kernel reduces into (sm_count_batch_multicast: multimem.red in the
-    epilogue, the all-reduce fused into the search).  `available` is False when the
+    address sm_count_batch_multicast reduces into (one multimem.red per pattern after the
+    search launches: the all-reduce done by the switch, no NCCL call).  `available` is False when the
     platform gives no multicast pointer (e.g. a single-GPU box, where cuMulticastCreate is
     refused); count_sharded_fused then uses count_sharded's NCCL all-reduce instead."""
 
