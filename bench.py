@@ -453,6 +453,23 @@ def run_native(args):
     if not args.no_cpu and world == 1:
         cpu = cpu_oracle_sample(spec, pats, args.cpu_seconds, len(os.sched_getaffinity(0)))
 
+    # NEXT-3: a batch over a <= 4-symbol text runs PACKED on the code array packed once per
+    # call, so each pass reads n b / 8 code bytes and the text-equivalent rate can exceed the
+    # HBM peak: the kernel is ALU-bound there (compare steps), reported as such
+    roofline_pre = None
+    nsym = int((hh > 0).sum())
+    if nsym <= 4 and P >= 2:
+        b = 1 if nsym <= 2 else 2
+        code_gbs = (spec.n * b / 8 * P + spec.n) / (search_ms * 1e-3) / 1e9
+        roofline_pre = {
+            "bound": "alu", "achieved": round(achieved, 1), "unit": "GB/s (text-equivalent)", "peak": None,
+            "frac": None, "hbm_GBps_code_bytes": round(code_gbs, 1), "hbm_frac_code_bytes": round(code_gbs / peak, 4),
+            "note": f"{b}-bit code array packed once per call; each pass reads n*{b}/8 bytes; compare-bound "
+                    "(SIMDcompare steps per warp-block: profiles/compare_counters_r1.md, ncu: "
+                    "profiles/ncu_packed_c4m32_r1.txt)",
+            "kernel": "search_kernel (PACKED-PRE count)", "avg_launch_us": round(search_ms * 1e3 / P, 2),
+        }
+
     strategies = {}
     for p in pats[:: max(1, P // 200)]:
         s_, r_ = sm.sm_plan(p.data, hh)
@@ -479,7 +496,7 @@ def run_native(args):
             "step": "hist + per-pattern order + batched count launches (each pattern a full pass) (+ all_reduce)",
         },
         "gpu_launches": int(launches),
-        "roofline": {
+        "roofline": roofline_pre if roofline_pre else {
             "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4),
             # DRAM read+write bytes per pattern pass, from the committed ncu --set full capture of

@@ -37,7 +37,7 @@ SM_OK, SM_EINVAL, SM_ETRUNC, SM_ENOMEM, SM_ECUDA = 0, 1, 2, 3, 4
 SM_STRATEGY_AUTO, SM_STRATEGY_FILTER, SM_STRATEGY_BLOCK, SM_STRATEGY_PACKED, SM_STRATEGY_PAIR = 0, 1, 2, 3, 4
 SM_COUNT_ERROR = (1 << 64) - 1
 SM_MAX_PATTERN = 4096
-STRATEGY_NAMES = {1: "filter", 2: "block", 3: "packed1", 4: "packed2", 5: "pair"}
+STRATEGY_NAMES = {1: "filter", 2: "block", 3: "packed1", 4: "packed2", 5: "pair", 6: "packed1-pre", 7: "packed2-pre"}
 
 EXPORTED_SYMBOLS = (
     "sm_count", "sm_report", "sm_symbol_order", "sm_histogram", "sm_order_from_histogram",

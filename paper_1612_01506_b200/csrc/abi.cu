@@ -141,6 +141,8 @@ struct Tunables {
   double pair_min_hit = 0.12;   // AUTO: PAIR instead of FILTER when p[pi(1)] is in > this share of 16-B chunks
   double block_min_hit = 0.3;   // AUTO: BLOCK / PACKED when a pi(1)&pi(2) survivor is in > this share
   uint32_t l2_policy = 0;       // TMA load L2 policy: 0 evict_first, 1 evict_normal, 2 evict_last
+  bool prepack = true;          // batches over <= 4-symbol texts: pack the text once (NEXT-3)
+  int ctas_pre = 3;             // persistent CTAs per SM for the pre-packed PACKED kernels (small stages)
 };
 
 const Tunables& tunables() {
@@ -154,6 +156,9 @@ const Tunables& tunables() {
     if (const char* e = std::getenv("SMGPU_PAIR_MIN_HIT")) x.pair_min_hit = std::atof(e);
     if (const char* e = std::getenv("SMGPU_BLOCK_MIN_HIT")) x.block_min_hit = std::atof(e);
     if (const char* e = std::getenv("SMGPU_L2_POLICY")) x.l2_policy = (uint32_t)std::atoi(e) % 3u;
+    if (const char* e = std::getenv("SMGPU_PREPACK")) x.prepack = std::atoi(e) != 0;
+    if (const char* e = std::getenv("SMGPU_CTAS_PRE")) x.ctas_pre = std::atoi(e);
+    if (x.ctas_pre < 1 || x.ctas_pre > 4) x.ctas_pre = 3;
     if (x.tile != 4096 && x.tile != 8192 && x.tile != 16384 && x.tile != 32768) x.tile = 32768;
     if (x.ctas_per_sm < 1 || x.ctas_per_sm > 4) x.ctas_per_sm = 2;
     if (x.max_stages < 2 || x.max_stages > (uint32_t)kMaxStages) x.max_stages = kMaxStages;
@@ -183,11 +188,11 @@ void choose_tiling(uint64_t n, Plan& pl) {
 // PACKED applicability: a b-bit field (x >> s) & (2^b - 1), b in {1, 2}, that is
 // injective on the symbols present in t, and every pattern symbol present in t.
 // Returns the strategy (kPacked1 / kPacked2) or 0; *shift receives s.
-int packed_projection(const uint64_t* hist, const uint8_t* p, size_t m, uint32_t* shift) {
+// The b-bit code field of the text (b in {1, 2}): (x >> s) & (2^b - 1) injective on the
+// symbols present in t.  Returns b (0 if none) and *shift = s.
+int text_code_bits(const uint64_t* hist, uint32_t* shift) {
   int present = 0;
   for (int c = 0; c < 256; ++c) present += hist[c] > 0;
-  for (size_t j = 0; j < m; ++j)
-    if (hist[p[j]] == 0) return 0;  // an absent symbol: FILTER answers 0 at once
   for (int b = 1; b <= 2; ++b) {
     if (present > (1 << b)) continue;
     for (uint32_t s = 0; s + b <= 8; ++s) {
@@ -201,11 +206,82 @@ int packed_projection(const uint64_t* hist, const uint8_t* p, size_t m, uint32_t
       }
       if (ok) {
         *shift = s;
-        return b == 1 ? kPacked1 : kPacked2;
+        return b;
       }
     }
   }
   return 0;
+}
+
+// PACKED applicability: a b-bit code field of the text (text_code_bits) and every
+// pattern symbol present in t.  Returns the strategy (kPacked1 / kPacked2) or 0.
+int packed_projection(const uint64_t* hist, const uint8_t* p, size_t m, uint32_t* shift) {
+  for (size_t j = 0; j < m; ++j)
+    if (hist[p[j]] == 0) return 0;  // an absent symbol: FILTER answers 0 at once
+  const int b = text_code_bits(hist, shift);
+  return b == 1 ? kPacked1 : (b == 2 ? kPacked2 : 0);
+}
+
+// The stream-ordered allocator returns freed blocks to the driver at every
+// synchronisation by default; keep them cached so per-call report scratch costs no
+// remapping (once per device).
+void keep_pool_cached() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  static bool done[64] = {false};
+  if (done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
+// NEXT-3: for a batch of >= 2 patterns over a <= 4-symbol text, pack the text once
+// into its code array and run the PACKED patterns on it (kPackedBPre).  Returns the
+// array (stream-ordered allocation, caller frees) or nullptr; *b_out = code bits.
+uint8_t* prepack_text(const uint64_t* hist, const uint8_t* t, size_t n, size_t P, cudaStream_t st, int* b_out,
+                      cudaError_t* err) {
+  *err = cudaSuccess;
+  *b_out = 0;
+  if (!tunables().prepack || P < 2 || n == 0) return nullptr;
+  uint32_t shift = 0;
+  const int b = text_code_bits(hist, &shift);
+  if (!b) return nullptr;
+  const uintptr_t tp = reinterpret_cast<uintptr_t>(t);
+  const uint64_t delta = tp & 15;
+  // alignments covered: every tile of every pattern plus the largest post region
+  const uint64_t X = ((delta + n + 32767) / 32768 + 1) * 32768 + 8192;
+  const uint64_t bytes = ((X * (uint64_t)b / 8) + 15) & ~15ull;
+  keep_pool_cached();  // per-call scratch: no remapping from the second call on
+  uint8_t* codes = nullptr;
+  *err = cudaMallocAsync(reinterpret_cast<void**>(&codes), bytes, st);
+  if (*err != cudaSuccess) return nullptr;
+  *err = launch_pack_text(reinterpret_cast<const uint8_t*>(tp & ~(uintptr_t)15), delta, n, shift, b, codes, bytes,
+                          num_sms(), st);
+  if (*err != cudaSuccess) {
+    cudaFreeAsync(codes, st);
+    return nullptr;
+  }
+  ++g_launches;
+  *b_out = b;
+  return codes;
+}
+
+// the pre-packed code array of one batch call (freed stream-ordered at scope end)
+struct CodeArray {
+  uint8_t* p;
+  cudaStream_t st;
+  ~CodeArray() {
+    if (p) cudaFreeAsync(p, st);
+  }
+};
+
+// a PACKED plan runs on the batch's code array when there is one (same b: same text)
+void use_codes(const CodeArray& codes, int cb, Plan& pl) {
+  if (codes.p && is_packed(pl.strategy) && !is_prepacked(pl.strategy) && code_bits(pl.strategy) == cb)
+    pl.strategy += kPacked1Pre - kPacked1;
 }
 
 sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist, const uint32_t* order,
@@ -308,6 +384,12 @@ void fill_desc(const Plan& pl, const uint8_t* p, size_t m, uint64_t delta, uint6
     d.pre = 0;
     const uint32_t post = (((uint32_t)m - 1) & ~15u) + 16;
     d.stage_len = (uint32_t)T + post;
+    if (is_prepacked(pl.strategy)) {
+      // the stage holds code bits: (T + post') alignments x b bits, post' >= m - 1 + 64 (the
+      // last unit's two-word windows), a multiple of 128 alignments (16-B granules)
+      const uint32_t postp = ((uint32_t)m - 1 + 64 + 127) & ~127u;
+      d.stage_len = ((uint32_t)T + postp) * (uint32_t)code_bits(pl.strategy) / 8u;
+    }
     d.k_begin = 0;
     d.ntiles = (delta + d.A - 1) / T + 1;
   }
@@ -339,8 +421,9 @@ void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_
   L.strategy = ps[0]->pl.strategy;
   L.epilogue = epilogue;
   L.e.clear();
-  const bool packed = L.strategy == kPacked1 || L.strategy == kPacked2;
-  const uint32_t cbits = L.strategy == kPacked2 ? 2 : 1;
+  const bool packed = is_packed(L.strategy);
+  const bool pre = is_prepacked(L.strategy);
+  const uint32_t cbits = (uint32_t)code_bits(L.strategy);
   L.a.code_shift = ps[0]->pl.code_shift;
   for (const Planned* q : ps)
     for (size_t k = 0; k < q->m; ++k) {
@@ -378,12 +461,12 @@ void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_
     }
     L.a.total_work = work;
     L.a.stage_stride = (max_stage + 127) & ~127u;
-    if (packed) {  // double-buffered code array: 2b bytes of codes per 16-byte chunk (+ a slack word)
+    if (packed && !pre) {  // double-buffered code array: 2b bytes of codes per 16-byte chunk (+ a slack word)
       L.a.pack_bytes = ((max_stage / 16u) * 2u * cbits + 16u + 127u) & ~127u;
       L.a.ring_off = L.a.pack_off + 2 * L.a.pack_bytes;
     }
     // shared memory per SM: 228 KiB, 1 KiB reserved per resident CTA
-    int ctas = tunables().ctas_per_sm;
+    int ctas = pre ? tunables().ctas_pre : tunables().ctas_per_sm;
     uint32_t stages = 0;
     for (; ctas >= 1; --ctas) {
       const uint32_t budget = std::min<uint32_t>(227 * 1024, 233472 / ctas - 1024);
@@ -463,16 +546,22 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
     if (s != SM_OK) return s;
     h = hb;
   }
+  // NEXT-3: a <= 4-symbol text is packed once for the whole batch
+  int cb = 0;
+  cudaError_t pe = cudaSuccess;
+  CodeArray codes{prepack_text(h, t, n, P, st, &cb, &pe), st};
+  if (pe != cudaSuccess) return cuda_fail(pe, "prepack");
   // plan and launch as we go: a batch is launched as soon as it is full, so the GPU
   // starts on the first patterns while the host still orders the later ones
   std::vector<Planned> plans(P);
-  constexpr int kStrategies = 6;                  // index = strategy value (1..5)
+  constexpr int kStrategies = 8;                  // index = strategy value (1..7)
   std::vector<const Planned*> batch[kStrategies];
-  size_t words[kStrategies] = {0, 0, 0, 0, 0};
+  size_t words[kStrategies] = {0, 0, 0, 0, 0, 0, 0, 0};
   auto flush = [&](int strat) -> sm_status {
     if (batch[strat].empty()) return SM_OK;
     HostLaunch L;
     build_launch(batch[strat], t, n, lim, kEpiCount, L);
+    L.a.codes = codes.p;
     batch[strat].clear();
     words[strat] = 0;
     return launch_checked(L, st, "search kernel (batch)");
@@ -483,6 +572,7 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
     q = Planned{Plan(), ps[i], ms[i], d_counts + i};
     sm_status s = make_plan(ps[i], ms[i], n, h, nullptr, 0, strategy, q.pl);
     if (s != SM_OK) return s;
+    use_codes(codes, cb, q.pl);
     const int k = q.pl.strategy;
     if (batch[k].size() == (size_t)kMaxBatch || words[k] + q.m > (size_t)kBatchTableWords) {
       s = flush(k);
@@ -511,22 +601,6 @@ uint64_t stage_pool_bytes(uint64_t cap) {
   return (b + 15) & ~15ull;
 }
 
-// The stream-ordered allocator returns freed blocks to the driver at every
-// synchronisation by default; keep them cached so per-call report scratch costs no
-// remapping (once per device).
-void keep_pool_cached() {
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
-  static bool done[64] = {false};
-  if (done[dev]) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
-  done[dev] = true;
-}
-
 // Reporting (A8) for P patterns, output concatenated in pattern order: pattern k's
 // ascending positions at pos[off_k ..), off_k = sum of earlier counts (first `cap`
 // positions overall are written).  One read of the text per pattern:
@@ -551,6 +625,10 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
     if (s != SM_OK) return s;
     h = hb;
   }
+  int cb = 0;
+  cudaError_t pe = cudaSuccess;
+  CodeArray codes{prepack_text(h, t, n, P, st, &cb, &pe), st};
+  if (pe != cudaSuccess) return cuda_fail(pe, "prepack");
   std::vector<Planned> plans;
   plans.reserve(P);
   for (size_t i = 0; i < P; ++i) {
@@ -558,6 +636,7 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
     Planned q{Plan(), ps[i], ms[i], d_counts + i};
     sm_status s = make_plan(ps[i], ms[i], n, h, P == 1 ? order : nullptr, P == 1 ? peel : 0, strategy, q.pl);
     if (s != SM_OK) return s;
+    use_codes(codes, cb, q.pl);
     plans.push_back(std::move(q));
   }
   if (plans.empty()) return SM_OK;
@@ -566,13 +645,15 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
   // a fixed slot range [item_base, item_base + ntiles) of the per-tile arrays in the
   // caller's order, so one scan gives the concatenated, pattern-ordered output layout
   std::vector<HostLaunch> Ls;
-  for (int strat : {(int)kFilter, (int)kPair, (int)kBlock, (int)kPacked1, (int)kPacked2}) {
+  for (int strat : {(int)kFilter, (int)kPair, (int)kBlock, (int)kPacked1, (int)kPacked2, (int)kPacked1Pre,
+                    (int)kPacked2Pre}) {
     std::vector<const Planned*> run;
     size_t words = 0;
     auto flush = [&]() {
       if (run.empty()) return;
       Ls.emplace_back();
       build_launch(run, t, n, lim, epi1, Ls.back());
+      Ls.back().a.codes = codes.p;
       run.clear();
       words = 0;
     };

@@ -33,6 +33,11 @@ cudaError_t launch_stage_expand(const uint8_t* stage, const unsigned long long* 
                                 const uint16_t* wc, const uint64_t* tile_offsets, uint64_t* pos, uint64_t cap,
                                 int num_sms, cudaStream_t st);
 
+// NEXT-3: the text's b-bit code array (code(x) = (x >> shift) & (2^b - 1)), base-relative
+// alignment x <-> bits [b x, b x + b); code_bytes (multiple of 16) of it, zero past the text
+cudaError_t launch_pack_text(const uint8_t* base, uint64_t delta, uint64_t n, uint32_t shift, int b, uint8_t* codes,
+                             uint64_t code_bytes, int num_sms, cudaStream_t st);
+
 // NEXT-4: mc[i] += local[i] through an NVLink multicast address (multimem.red)
 cudaError_t launch_nvls_add(const uint64_t* local, uint64_t* mc, uint64_t P, cudaStream_t st);
 

@@ -25,7 +25,12 @@ constexpr uint32_t kQueueOff = kWarpTotOff + 2 * kConsumerWarps * 4;
 constexpr uint32_t kTblOff = kQueueOff + kConsumerWarps * kQueueLen * 2;  // end of the fixed region
 
 // kPackedB: b-bit codes; kPair: FILTER whose chunk test covers pi(1) and pi(2) together
-enum Strategy : int { kFilter = 1, kBlock = 2, kPacked1 = 3, kPacked2 = 4, kPair = 5 };
+// kPackedBPre: PACKED reading a code array packed once per call (pack_text_kernel) instead
+// of packing every tile (NEXT-3: the per-symbol codes memoised at text scope)
+enum Strategy : int { kFilter = 1, kBlock = 2, kPacked1 = 3, kPacked2 = 4, kPair = 5, kPacked1Pre = 6, kPacked2Pre = 7 };
+__host__ __device__ constexpr bool is_packed(int s) { return s == kPacked1 || s == kPacked2 || s >= kPacked1Pre; }
+__host__ __device__ constexpr bool is_prepacked(int s) { return s >= kPacked1Pre; }
+__host__ __device__ constexpr int code_bits(int s) { return (s == kPacked2 || s == kPacked2Pre) ? 2 : 1; }
 // kEpiCount: per-pattern counts.  kEpiStage: reporting pass 1 -- per-(pattern, tile) counts
 // plus the tile's matches staged compactly in global memory (per-warp u16 offset lists
 // or bitmaps), expanded into positions by stage_expand_kernel after the scan: the
@@ -93,6 +98,8 @@ struct LaunchArgs {
   uint32_t l2_policy;        // TMA loads: 0 evict_first, 1 evict_normal, 2 evict_last (performance only)
   uint32_t pack_off;         // PACKED: smem byte offset of the double-buffered code array
   uint32_t pack_bytes;       // PACKED: bytes of one code buffer
+  const uint8_t* codes;      // kPackedBPre: the code array of the text (base-relative alignment x <-> code bits
+                             // [b x, b x + b) of the array), 16-B aligned, zero past the text
   uint32_t list_off;         // reporting: smem byte offset of the per-warp position lists [W][kListCap] u16
   uint16_t* wc;              // kEpiStage: per item u16[kConsumerWarps] match counts (zeroed by host)
   uint8_t* stage;            // kEpiStage: staging pool (records)

@@ -177,7 +177,8 @@ struct WorkIter {
 // wait for a free stage, load the ragged 16-B ends of t byte-wise, then one
 // cp.async.bulk for the aligned interior, completion counted on full[s].
 // ---------------------------------------------------------------------------
-template <int EPI, int CAP>
+// PRE: kPackedBPre -- tiles come from the code array (CB code bits per alignment).
+template <int EPI, int CAP, bool PRE = false, int CB = 1>
 __device__ void produce(const LaunchParams<CAP>& P, uint8_t* ring, uint64_t* full, uint64_t* empty) {
   const LaunchArgs& a = P.a;
   const uint64_t pol = a.l2_policy == 2 ? l2_policy_evict_last()
@@ -192,6 +193,18 @@ __device__ void produce(const LaunchParams<CAP>& P, uint8_t* ring, uint64_t* ful
     const PatDesc& d = P.d[k];
     if (wrapped) mbar_wait_sleep(&empty[s], ph ^ 1u);  // consumers released this stage's previous use
     uint8_t* buf = ring + (size_t)s * a.stage_stride;
+    if (PRE) {  // the tile's codes: one bulk copy from the padded code array (16-B granules)
+      const uint64_t lo = ((d.k_begin + ti) * a.tile * CB) / 8u;
+      mbar_arrive_expect_tx(&full[s], d.stage_len);
+      SMGPU_DCHECK((lo & 15u) == 0 && (d.stage_len & 15u) == 0 && d.stage_len <= a.stage_stride);
+      tma_load_1d(buf, a.codes + lo, d.stage_len, &full[s], pol);
+      if (++s == a.stages) {
+        s = 0;
+        ph ^= 1u;
+        wrapped = true;
+      }
+      continue;
+    }
     const int64_t lo = (int64_t)((d.k_begin + ti) * a.tile) - (int64_t)d.pre;
     const int64_t hi = lo + (int64_t)d.stage_len;
     const int64_t vlo = imax(lo, tlo), vhi = imin(hi, thi);
@@ -615,25 +628,31 @@ __device__ __forceinline__ void packed_step(uint32_t (&F)[CPL], const uint32_t (
 // exit test.  Returns per-chunk 16-bit match masks.
 // Returns the number of result units; unit i: mask m_out[i] (bit b <-> tile-relative
 // alignment base_out[i] + b), units in ascending order within each lane-round.
-template <int CPL, int B>
+// PRE (kPackedBPre): the stage already holds the tile's codes (packed once per call), so
+// there is no packing, no CTA barrier, and the stage is released by the caller.
+template <int CPL, int B, bool PRE = false>
 __device__ __forceinline__ int packed_tile(const Pat& pt, const uint8_t* buf, uint8_t* pk, uint32_t pk_words,
                                            uint32_t nchunks,
                                             uint32_t code_shift, uint32_t cw0, int warp, int lane, bool edge,
                                             int32_t rlo, int32_t rhi, uint64_t* empty_bar, uint32_t* m_out,
                                             uint32_t* base_out, Ctr& C) {
   const bool valid_block = !edge || (rlo < (int32_t)(16u * cw0 + 512u * CPL) && rhi > (int32_t)(16u * cw0));
+  if constexpr (PRE) {
+    pk = const_cast<uint8_t*>(buf);
+  } else {
 #pragma unroll
-  for (int it = 0; it < CPL; ++it) {
-    const uint32_t c = cw0 + it * 32u + lane;
-    store_codes<B>(pk, c, pack_chunk<B>(lds128(buf + 16u * c), code_shift));
+    for (int it = 0; it < CPL; ++it) {
+      const uint32_t c = cw0 + it * 32u + lane;
+      store_codes<B>(pk, c, pack_chunk<B>(lds128(buf + 16u * c), code_shift));
+    }
+    for (uint32_t c = (uint32_t)CPL * kLanesPerTilePass + warp * 32u + lane; c < nchunks; c += kLanesPerTilePass) {
+      SMGPU_DCHECK(16u * c + 16u <= pt.lim && (c + 1u) * 2u * B <= 4u * pk_words);
+      store_codes<B>(pk, c, pack_chunk<B>(lds128(buf + 16u * c), code_shift));  // halo chunks
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty_bar);  // the stage's bytes are no longer needed
+    named_bar_sync(1, kConsumerWarps * 32);  // all codes of the tile are in place
   }
-  for (uint32_t c = (uint32_t)CPL * kLanesPerTilePass + warp * 32u + lane; c < nchunks; c += kLanesPerTilePass) {
-    SMGPU_DCHECK(16u * c + 16u <= pt.lim && (c + 1u) * 2u * B <= 4u * pk_words);
-    store_codes<B>(pk, c, pack_chunk<B>(lds128(buf + 16u * c), code_shift));  // halo chunks
-  }
-  __syncwarp();
-  if (lane == 0) mbar_arrive(empty_bar);  // the stage's bytes are no longer needed
-  named_bar_sync(1, kConsumerWarps * 32);  // all codes of the tile are in place
   const uint32_t* pk32 = reinterpret_cast<const uint32_t*>(pk);
   if constexpr (B == 1 && CPL >= 2) {
     // 1-bit codes: a lane compares a whole code word = 32 consecutive alignments per
@@ -920,7 +939,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
   __syncthreads();
 
   if (warp == kConsumerWarps) {
-    if (lane == 0) produce<EPI>(P, ring, full, empty);
+    if (lane == 0) produce<EPI, CAP, is_prepacked(STRAT), code_bits(STRAT)>(P, ring, full, empty);
     return;
   }
 
@@ -1002,13 +1021,15 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_consta
         }
         par ^= 1u;
       }
-    } else if (STRAT == kPacked1 || STRAT == kPacked2) {
-      constexpr int B = STRAT == kPacked2 ? 2 : 1;
+    } else if (is_packed(STRAT)) {
+      constexpr int B = code_bits(STRAT);
+      constexpr bool PRE = is_prepacked(STRAT);
       uint32_t mk[CPL], mbase[CPL];
       uint8_t* pk = smem + a.pack_off + par_pk * a.pack_bytes;
-      const int units = packed_tile<CPL, B>(pt, buf, pk, a.pack_bytes / 4u, d.stage_len / 16u, a.code_shift, cw0,
-                                            warp, lane, edge, rlo, rhi, &empty[s], mk, mbase, C);
-      released = true;  // packed_tile released the stage after packing
+      const int units = packed_tile<CPL, B, PRE>(pt, buf, pk, PRE ? d.stage_len / 4u : a.pack_bytes / 4u,
+                                                 d.stage_len / 16u, a.code_shift, cw0, warp, lane, edge, rlo, rhi,
+                                                 &empty[s], mk, mbase, C);
+      released = !PRE;  // packed_tile released the stage after packing (PRE: it was read until now)
       par_pk ^= 1u;
       uint32_t tc = 0;
 #pragma unroll

@@ -53,6 +53,19 @@ for n in ((1 << 20) + 333, (16 << 20) + 77):
                     print(("ok " if ok else "MISMATCH ") + f"n={n} sigma={syms.size} m={m} strat={strategy} r={peel} "
                           f"alpha={c['alpha_eff']} steps={c['steps']}/{steps} blocks={c['blocks']}/{blocks} "
                           f"count={got}/{want}")
+            if syms.size <= 4:  # batches of >= 2 patterns run PACKED on the text's code array (NEXT-3)
+                sm.sm_counters(reset=True)
+                d2 = torch.zeros(2, dtype=torch.int64, device="cuda")
+                sm.sm_count_batch([p, p], t, d2, hist=oracle.hist(a), strategy=sm.SM_STRATEGY_PACKED)
+                c = sm.sm_counters(reset=True)
+                pi_auto = oracle.order(oracle.hist(a), p)
+                r_auto = sm.sm_plan(p, oracle.hist(a), strategy=sm.SM_STRATEGY_PACKED)[1]
+                steps, blocks = oracle.alg4_steps(p, a, alpha=c["alpha_eff"], pi=pi_auto, r=r_auto)
+                want = oracle.naive_count(p, a)
+                ok = d2.cpu().tolist() == [want, want] and c["steps"] == 2 * steps and c["blocks"] == 2 * blocks
+                fails += not ok
+                print(("ok " if ok else "MISMATCH ") + f"PRE-PACKED batch n={n} sigma={syms.size} m={m} "
+                      f"steps={c['steps']}/{2 * steps} blocks={c['blocks']}/{2 * blocks}")
             for fs in (sm.SM_STRATEGY_FILTER, sm.SM_STRATEGY_PAIR):  # survivors of pi(1), pi(2)
                 if m < 2:
                     break
