@@ -90,6 +90,16 @@ def test_plan_auto_rule(sm):
     assert s == sm.SM_STRATEGY_FILTER              # PAIR needs pi(2): m = 1 runs FILTER
 
 
+def test_multicast_count_argument_checks(sm):
+    """sm_count_batch_multicast validates before touching the GPU (n = 0: no text check)."""
+    lib = sm.load_library()
+    pats = sm.PatternBatch([b"ab", b"c"])
+    args = (ctypes.addressof(pats.ptrs), ctypes.addressof(pats.lens), pats.P, None, 0, 2 ** 64 - 1, None, 0)
+    assert lib.sm_count_batch_multicast(*args, 0x1003, None) == sm.SM_EINVAL      # misaligned multicast address
+    assert lib.sm_count_batch_multicast(*args[:7], 9, 0x1000, None) == sm.SM_EINVAL  # bad strategy
+    assert lib.sm_count_batch_multicast(*args[:7], 0, None, None) == sm.SM_EINVAL    # NULL counts
+
+
 def test_argument_errors_without_gpu(sm):
     lib = sm.load_library()
     host = (ctypes.c_uint8 * 8)()
