@@ -30,8 +30,10 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # SMGPU_LIB=debug selects the bounds-checked build (libsmgpu_debug.so, tests only);
 # SMGPU_LIB=counters the compare-step instrumented build (libsmgpu_counters.so, NEXT-2)
+# (SMGPU_LIB=/path/to/lib.so loads another build of the same ABI: A/B measurements in tools/)
 _VARIANTS = {"debug": "libsmgpu_debug.so", "counters": "libsmgpu_counters.so"}
-LIB_PATH = os.path.join(_HERE, _VARIANTS.get(os.environ.get("SMGPU_LIB", ""), "libsmgpu.so"))
+_SEL = os.environ.get("SMGPU_LIB", "")
+LIB_PATH = _SEL if _SEL.endswith(".so") else os.path.join(_HERE, _VARIANTS.get(_SEL, "libsmgpu.so"))
 
 SM_OK, SM_EINVAL, SM_ETRUNC, SM_ENOMEM, SM_ECUDA = 0, 1, 2, 3, 4
 SM_STRATEGY_AUTO, SM_STRATEGY_FILTER, SM_STRATEGY_BLOCK, SM_STRATEGY_PACKED, SM_STRATEGY_PAIR = 0, 1, 2, 3, 4
