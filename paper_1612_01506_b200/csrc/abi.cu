@@ -143,6 +143,7 @@ struct Tunables {
   uint32_t l2_policy = 0;       // TMA load L2 policy: 0 evict_first, 1 evict_normal, 2 evict_last
   bool prepack = true;          // batches over <= 4-symbol texts: pack the text once (NEXT-3)
   int ctas_pre = 3;             // persistent CTAs per SM for the pre-packed PACKED kernels (small stages)
+  uint32_t max_stages_pre = 6;  // their ring depth (3 CTAs x 6 stages of <= 9 KiB fit the SM)
 };
 
 const Tunables& tunables() {
@@ -159,6 +160,8 @@ const Tunables& tunables() {
     if (const char* e = std::getenv("SMGPU_PREPACK")) x.prepack = std::atoi(e) != 0;
     if (const char* e = std::getenv("SMGPU_CTAS_PRE")) x.ctas_pre = std::atoi(e);
     if (x.ctas_pre < 1 || x.ctas_pre > 4) x.ctas_pre = 3;
+    if (const char* e = std::getenv("SMGPU_STAGES_PRE")) x.max_stages_pre = (uint32_t)std::atoi(e);
+    if (x.max_stages_pre < 2 || x.max_stages_pre > (uint32_t)kMaxStages) x.max_stages_pre = 6;
     if (x.tile != 4096 && x.tile != 8192 && x.tile != 16384 && x.tile != 32768) x.tile = 32768;
     if (x.ctas_per_sm < 1 || x.ctas_per_sm > 4) x.ctas_per_sm = 2;
     if (x.max_stages < 2 || x.max_stages > (uint32_t)kMaxStages) x.max_stages = kMaxStages;
@@ -492,7 +495,7 @@ void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_
         d.flags |= std::min<uint32_t>(r1, 255u) << 8;
       }
     }
-    L.a.stages = std::min<uint32_t>(stages, tunables().max_stages);
+    L.a.stages = std::min<uint32_t>(stages, pre ? tunables().max_stages_pre : tunables().max_stages);
     L.smem = (size_t)L.a.ring_off + (size_t)L.a.stages * L.a.stage_stride;
     const uint64_t sms = (uint64_t)num_sms();
     L.grid = (int)std::min<uint64_t>(work, sms * (uint64_t)ctas);

@@ -18,12 +18,30 @@ cudaError_t launch_one(const HostLaunch& L, cudaStream_t st) {
     if (err != cudaSuccess) return err;
     attr_done = true;
   }
+  // persistent grid: never more CTAs than can be resident at once (registers or shared
+  // memory may allow fewer per SM than the host's plan assumed) -- a second wave of CTAs
+  // would run the round-robin work items after the first, a tail of up to 50 %
+  int grid = L.grid;
+  {
+    static thread_local size_t cached_smem = ~(size_t)0;
+    static thread_local int cached_blocks = 0;
+    if (cached_smem != L.smem) {
+      int nb = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kfn, kThreads, L.smem) != cudaSuccess) nb = 0;
+      cached_smem = L.smem;
+      cached_blocks = nb;
+    }
+    int dev = 0, sms = 0;
+    if (cached_blocks > 0 && cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0)
+      grid = grid < cached_blocks * sms ? grid : cached_blocks * sms;
+  }
   static thread_local LaunchParams<CAP> P;  // ~19 KiB for CAP = 4096: keep it off the stack
   P.a = L.a;
   std::memset(P.d, 0, sizeof(P.d));
   std::memcpy(P.d, L.d.data(), L.d.size() * sizeof(PatDesc));
   std::memcpy(P.e, L.e.data(), L.e.size() * sizeof(uint32_t));
-  kfn<<<L.grid, kThreads, L.smem, st>>>(P);
+  kfn<<<grid, kThreads, L.smem, st>>>(P);
   return cudaGetLastError();
 }
 

@@ -919,8 +919,11 @@ __device__ __forceinline__ void stage_warp(const LaunchArgs& a, const PatDesc& d
 // = (pattern k, tile ti) in pattern-major order, round-robin over persistent CTAs
 // (one CTA flows from one pattern's last tiles into the next pattern's first).
 // ---------------------------------------------------------------------------
+// 2 CTAs per SM (shared memory: 3-stage rings of 32 KiB tiles); the pre-packed PACKED
+// kernels have small stages and are register-capped for 3
 template <int STRAT, int EPI, int CAP, int CPL>
-__global__ void __launch_bounds__(kThreads, 2) search_kernel(const __grid_constant__ LaunchParams<CAP> P) {
+__global__ void __launch_bounds__(kThreads, is_prepacked(STRAT) ? 3 : 2)
+    search_kernel(const __grid_constant__ LaunchParams<CAP> P) {
   extern __shared__ __align__(128) uint8_t smem[];
   const LaunchArgs& a = P.a;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
