@@ -134,7 +134,8 @@ bool valid_permutation(const uint32_t* order, size_t m) {
 // variables override them once per process for tuning sweeps.
 struct Tunables {
   uint32_t tile = 32768;        // text bytes per tile for large texts (4096 * CPL)
-  int ctas_per_sm = 2;          // persistent CTAs per SM
+  int ctas_per_sm = 3;          // persistent CTAs per SM (3 x 2 stages beat 2 x 3 stages by ~11 %: more
+                                // resident warps; the planner falls back to 2 when 2 stages do not fit)
   uint32_t max_stages = 8;      // ring depth cap per CTA
   bool auto_packed = true;      // AUTO may pick PACKED for small text alphabets
   bool alternate = true;        // batches: odd patterns scan the text backwards (L2 reuse at the seam)
@@ -163,7 +164,7 @@ const Tunables& tunables() {
     if (const char* e = std::getenv("SMGPU_STAGES_PRE")) x.max_stages_pre = (uint32_t)std::atoi(e);
     if (x.max_stages_pre < 2 || x.max_stages_pre > (uint32_t)kMaxStages) x.max_stages_pre = 6;
     if (x.tile != 4096 && x.tile != 8192 && x.tile != 16384 && x.tile != 32768) x.tile = 32768;
-    if (x.ctas_per_sm < 1 || x.ctas_per_sm > 4) x.ctas_per_sm = 2;
+    if (x.ctas_per_sm < 1 || x.ctas_per_sm > 4) x.ctas_per_sm = 3;
     if (x.max_stages < 2 || x.max_stages > (uint32_t)kMaxStages) x.max_stages = kMaxStages;
     return x;
   }();
