@@ -441,7 +441,11 @@ void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_
   L.a.l2_policy = tunables().l2_policy;
   // reporting launches reserve the per-warp position lists
   L.a.list_off = (kTblOff + 127) & ~127u;
-  const uint32_t list_bytes = epilogue == kEpiCount ? 0u : (uint32_t)(kConsumerWarps * kListCap * 2);
+  // reporting: kEpiStage keeps one 32 CPL-mask bitmap per warp (<= 512 B), the overflow
+  // pass (kEpiWrite) a kListCap-entry position list per warp
+  const uint32_t list_bytes = epilogue == kEpiCount ? 0u
+                              : epilogue == kEpiStage ? (uint32_t)(kConsumerWarps * 32 * 8 * 2)
+                                                      : (uint32_t)(kConsumerWarps * kListCap * 2);
   L.a.pack_off = (L.a.list_off + list_bytes + 127) & ~127u;
   L.a.ring_off = L.a.pack_off;
   uint32_t T = ps[0]->pl.tile;
@@ -649,6 +653,7 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
   // a fixed slot range [item_base, item_base + ntiles) of the per-tile arrays in the
   // caller's order, so one scan gives the concatenated, pattern-ordered output layout
   std::vector<HostLaunch> Ls;
+  std::vector<std::vector<const Planned*>> runs;  // each launch's patterns (the overflow pass rebuilds)
   for (int strat : {(int)kFilter, (int)kPair, (int)kBlock, (int)kPacked1, (int)kPacked2, (int)kPacked1Pre,
                     (int)kPacked2Pre}) {
     std::vector<const Planned*> run;
@@ -658,6 +663,7 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
       Ls.emplace_back();
       build_launch(run, t, n, lim, epi1, Ls.back());
       Ls.back().a.codes = codes.p;
+      runs.push_back(run);
       run.clear();
       words = 0;
     };
@@ -733,13 +739,20 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
     e = launch_stage_expand(stage, stage_used, stage_b / 16, wc, offsets, pos, cap, num_sms(), st);
     if (e == cudaSuccess) ++g_launches;
   }
-  for (HostLaunch& L : Ls) {  // overflow pass (CTAs exit at once when the queue is empty)
+  for (size_t li = 0; li < Ls.size(); ++li) {  // overflow pass (CTAs exit at once when the queue is empty)
     if (e != cudaSuccess) break;
-    L.epilogue = kEpiWrite;
-    L.a.tile_offsets = offsets;
-    L.a.pos = pos;
-    L.a.cap = cap;
-    e = launch_search(L, st);
+    HostLaunch W;  // its own shared-memory layout (position lists), same patterns and arguments
+    build_launch(runs[li], t, n, lim, kEpiWrite, W);
+    for (size_t i = 0; i < W.d.size(); ++i) W.d[i].item_base = Ls[li].d[i].item_base;
+    const LaunchArgs& a1 = Ls[li].a;
+    W.a.codes = a1.codes;
+    W.a.ovf_items = a1.ovf_items;
+    W.a.ovf_n = a1.ovf_n;
+    W.a.pos_offset = a1.pos_offset;
+    W.a.tile_offsets = offsets;
+    W.a.pos = pos;
+    W.a.cap = cap;
+    e = launch_search(W, st);
     if (e == cudaSuccess) ++g_launches;
   }
   cudaFreeAsync(scratch, st);

@@ -919,10 +919,10 @@ __device__ __forceinline__ void stage_warp(const LaunchArgs& a, const PatDesc& d
 // = (pattern k, tile ti) in pattern-major order, round-robin over persistent CTAs
 // (one CTA flows from one pattern's last tiles into the next pattern's first).
 // ---------------------------------------------------------------------------
-// 2 CTAs per SM (shared memory: 3-stage rings of 32 KiB tiles); the pre-packed PACKED
-// kernels have small stages and are register-capped for 3
+// 3 CTAs per SM (2-stage rings of 32 KiB tiles); the reporting stage pass and the
+// pre-packed PACKED kernels are register-capped for 3 too
 template <int STRAT, int EPI, int CAP, int CPL>
-__global__ void __launch_bounds__(kThreads, is_prepacked(STRAT) ? 3 : 2)
+__global__ void __launch_bounds__(kThreads, (is_prepacked(STRAT) || EPI == kEpiStage) ? 3 : 2)
     search_kernel(const __grid_constant__ LaunchParams<CAP> P) {
   extern __shared__ __align__(128) uint8_t smem[];
   const LaunchArgs& a = P.a;
@@ -948,7 +948,7 @@ __global__ void __launch_bounds__(kThreads, is_prepacked(STRAT) ? 3 : 2)
 
   uint16_t* qc = reinterpret_cast<uint16_t*>(smem + kQueueOff) + warp * kQueueLen;
   // reporting only: kEpiWrite position list (kListCap u16) / kEpiStage bitmap (32 CPL u16)
-  uint16_t* list = reinterpret_cast<uint16_t*>(smem + a.list_off) + warp * kListCap;
+  uint16_t* list = reinterpret_cast<uint16_t*>(smem + a.list_off) + warp * (EPI == kEpiWrite ? kListCap : 32 * CPL);
   StageAlloc salloc;     // kEpiStage: this warp's staging-pool chunk
   if (EPI == kEpiStage) {  // the bitmap starts clean
     uint32_t* bw = reinterpret_cast<uint32_t*>(list);
