@@ -414,7 +414,7 @@ struct Planned {
 
 // Build one launch over patterns `ps` (same strategy; <= kMaxBatch, table <= kTableLarge).
 // The tile is the plan's (large texts: 32 KiB); the batching loops keep a launch's
-// table <= kBatchTableWords so that 3 stages fit; T is halved only if fewer than 2 do.
+// table <= kBatchTableWords; T is halved only if fewer than 2 stages fit.
 void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_t n, uint64_t lim, int epilogue,
                   HostLaunch& L) {
   const uintptr_t tp = reinterpret_cast<uintptr_t>(t);

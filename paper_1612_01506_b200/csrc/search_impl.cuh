@@ -2,12 +2,12 @@
 // patterns in a device-resident byte text, pattern symbols compared rarest-first
 // with peeled first comparisons (Algs. 3-4), B200-native.
 //
-// Persistent CTAs (2 per SM): warp 8 is the TMA producer, warps 0..7 compare.
+// Persistent CTAs (3 per SM): warp 8 is the TMA producer, warps 0..7 compare.
 // A launch runs a batch of patterns; each pattern is a full pass over the text.
 //   * A3 staging (the paper loads 16/32 unaligned bytes): tiles
 //     of T = 32 KiB plus the pattern's halo are copied HBM -> shared memory with
 //     1-D TMA bulk copies (cp.async.bulk, 16-B granules, L2 evict-first) into a
-//     3-stage ring of mbarrier-guarded buffers.  Ragged 16-B ends of the text are
+//     ring (2-3 stages) of mbarrier-guarded buffers.  Ragged 16-B ends of the text are
 //     loaded byte-wise by the producer, so nothing outside t[0..n) is read.
 //   * SIMDcompare becomes a packed-byte compare: a lane owns
 //     chunks of 16 consecutive alignments held as 4 x u32 words, one flag bit
