@@ -139,8 +139,8 @@ struct Tunables {
   uint32_t max_stages = 8;      // ring depth cap per CTA
   bool auto_packed = true;      // AUTO may pick PACKED for small text alphabets
   bool alternate = true;        // batches: odd patterns scan the text backwards (L2 reuse at the seam)
-  double pair_min_hit = 0.12;   // AUTO: PAIR instead of FILTER when p[pi(1)] is in > this share of 16-B chunks
-  double block_min_hit = 0.3;   // AUTO: BLOCK / PACKED when a pi(1)&pi(2) survivor is in > this share
+  double pair_min_hit = 0.2;    // AUTO: PAIR instead of FILTER when p[pi(1)] is in > this share of 16-B chunks
+  double block_min_hit = 0.5;   // AUTO: BLOCK / PACKED when a pi(1)&pi(2) survivor is in > this share
   uint32_t l2_policy = 0;       // TMA load L2 policy: 0 evict_first, 1 evict_normal, 2 evict_last
   bool prepack = true;          // batches over <= 4-symbol texts: pack the text once (NEXT-3)
   int ctas_pre = 3;             // persistent CTAs per SM for the pre-packed PACKED kernels (small stages)

@@ -65,8 +65,8 @@ def test_plan_policy(sm):
 
 def test_plan_auto_rule(sm):
     """AUTO (abi.cu make_plan, profiles/strategy_pair_r1.md): h1 = 1-(1-f1)^16 is FILTER's chunk
-    queue rate, h12 = 1-(1-f1 f2)^16 PAIR's (h1 for m = 1); BLOCK/PACKED if h12 > 0.3, else PAIR
-    if m >= 2 and h1 > 0.12, else FILTER."""
+    queue rate, h12 = 1-(1-f1 f2)^16 PAIR's (h1 for m = 1); BLOCK/PACKED if h12 > 0.5, else PAIR
+    if m >= 2 and h1 > 0.2, else FILTER."""
     h = np.zeros(256, dtype=np.uint64)
     # 20 symbols 'A'..'T': two frequent (10 % each), the rest rare
     for i, c in enumerate(range(65, 85)):
@@ -74,16 +74,18 @@ def test_plan_auto_rule(sm):
     rare, freq = b"T", b"A"
     s, _ = sm.sm_plan(rare + freq * 3, h)          # f1 ~ 4.9 %: h1 ~ 0.55 > 0.12, h12 ~ 0.08 -> PAIR
     assert s == 5 and sm.STRATEGY_NAMES[s] == "pair"
-    s, _ = sm.sm_plan(rare, h)                     # m = 1: h12 := h1 ~ 0.51 > 0.3 -> BLOCK
+    s, _ = sm.sm_plan(rare, h)                     # m = 1: h12 := h1 ~ 0.51 > 0.5 -> BLOCK
     assert s == sm.SM_STRATEGY_BLOCK
     h[ord("T")] = 10                               # a rare pi(1): h1 ~ 0.9 %: FILTER
     s, _ = sm.sm_plan(b"T" + freq * 3, h)
     assert s == sm.SM_STRATEGY_FILTER
     hb = np.zeros(256, dtype=np.uint64)
-    for c in range(65, 70):                        # 5 equally frequent symbols: h12 = 1-(1-1/25)^16 ~ 0.48
-        hb[c] = 1000
-    s, _ = sm.sm_plan(b"ABCDE", hb)
-    assert s == sm.SM_STRATEGY_BLOCK               # 5 symbols: no 2-bit code -> BLOCK
+    for c in range(65, 71):                        # 6 symbols, 'A' and 'B' 45 % each
+        hb[c] = 9000 if c < 67 else 500
+    s, _ = sm.sm_plan(b"ABAB", hb)                 # h12 = 1-(1-0.2025)^16 ~ 0.97 > 0.5
+    assert s == sm.SM_STRATEGY_BLOCK               # 6 symbols: no 2-bit code -> BLOCK
+    s, _ = sm.sm_plan(b"ABCDE", hb)                # pi(1), pi(2) = C, D (5 % each): h1 ~ 0.56 -> PAIR
+    assert s == 5
     s, _ = sm.sm_plan(b"ABCDE", hb, strategy=sm.SM_STRATEGY_PAIR)
     assert s == 5                                  # forced
     s, _ = sm.sm_plan(b"A", hb, strategy=sm.SM_STRATEGY_PAIR)
