@@ -147,7 +147,11 @@ sm_status sm_count_async(const uint8_t* p, size_t m, const uint8_t* t, size_t n,
  * full pass over the text (no sharing of reads between patterns); batching only
  * lets the persistent kernel flow from one pattern's last tiles into the next
  * pattern's first tiles and amortises launch overhead.  hist: as in
- * sm_count_async; order and peeling factor are chosen per pattern (AUTO). */
+ * sm_count_async; order and peeling factor are chosen per pattern (AUTO).
+ * Scratch: for P >= 2 over a text with <= 4 distinct symbols the call packs the
+ * text once into a temporary b-bit code array (b = 1 or 2; ~n b / 8 bytes from the
+ * stream-ordered pool, freed on the stream) that the PACKED passes read instead of
+ * the bytes (SMGPU_PREPACK=0 disables). */
 sm_status sm_count_batch(const uint8_t* const* p, const size_t* m, size_t P, const uint8_t* t, size_t n,
                          size_t max_alignments, const uint64_t* hist, int strategy, uint64_t* d_counts,
                          void* stream);
@@ -177,7 +181,11 @@ sm_status sm_report_async(const uint8_t* p, size_t m, const uint8_t* t, size_t n
                           void* stream);
 
 /* Enqueue the reporting version for P patterns (see sm_count_batch for p, m,
- * max_alignments, hist, strategy).  d_counts[i] (DEVICE u64[P]) = count of p[i];
+ * max_alignments, hist, strategy, and the code-array scratch).  One read of the text
+ * per pattern: matches are staged compactly (scratch from the stream-ordered pool:
+ * ~24 B per (pattern, 32 KiB tile) plus a staging pool of min(2 GiB, 64 MiB + 4 cap)
+ * bytes, SMGPU_STAGE_BYTES overrides), then expanded; tiles that do not fit the pool
+ * are recomputed from the text -- never a different result.  d_counts[i] (DEVICE u64[P]) = count of p[i];
  * positions of all patterns are written CONCATENATED in pattern order into DEVICE
  * pos[0..cap): pattern i's ascending positions start at sum_{j<i} d_counts[j].
  * Positions past cap are dropped (the caller detects truncation from d_counts).
