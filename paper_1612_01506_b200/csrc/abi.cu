@@ -101,6 +101,18 @@ sm_status check_pattern_text(const uint8_t* p, size_t m, const uint8_t* t, size_
 // (at most 256 of them), then positions are bucketed by rank in ascending order.
 // O(m + 256 log 256); equals std::stable_sort by hist[p[j]].
 void order_from_hist(const uint64_t* hist, const uint8_t* p, size_t m, uint32_t* order) {
+  if (m <= 48) {  // short patterns: stable insertion sort of the positions by count
+    for (size_t j = 0; j < m; ++j) {
+      const uint64_t key = hist[p[j]];
+      size_t i = j;
+      while (i > 0 && hist[p[order[i - 1]]] > key) {
+        order[i] = order[i - 1];
+        --i;
+      }
+      order[i] = (uint32_t)j;
+    }
+    return;
+  }
   bool present[256] = {false};
   for (size_t j = 0; j < m; ++j) present[p[j]] = true;
   uint8_t syms[256];
@@ -217,14 +229,6 @@ int text_code_bits(const uint64_t* hist, uint32_t* shift) {
   return 0;
 }
 
-// PACKED applicability: a b-bit code field of the text (text_code_bits) and every
-// pattern symbol present in t.  Returns the strategy (kPacked1 / kPacked2) or 0.
-int packed_projection(const uint64_t* hist, const uint8_t* p, size_t m, uint32_t* shift) {
-  for (size_t j = 0; j < m; ++j)
-    if (hist[p[j]] == 0) return 0;  // an absent symbol: FILTER answers 0 at once
-  const int b = text_code_bits(hist, shift);
-  return b == 1 ? kPacked1 : (b == 2 ? kPacked2 : 0);
-}
 
 // The stream-ordered allocator returns freed blocks to the driver at every
 // synchronisation by default; keep them cached so per-call report scratch costs no
@@ -288,9 +292,37 @@ void use_codes(const CodeArray& codes, int cb, Plan& pl) {
     pl.strategy += kPacked1Pre - kPacked1;
 }
 
+// Per-text facts every plan of a call needs (computed once per call, not per pattern).
+struct TextInfo {
+  double total = 0;         // n from the histogram
+  int code_b = 0;           // text_code_bits: 0, 1 or 2
+  uint32_t code_shift = 0;
+  Plan tiling;              // choose_tiling(n): tile and CPL
+};
+
+TextInfo text_info(const uint64_t* hist, uint64_t n) {
+  TextInfo t;
+  for (int c = 0; c < 256; ++c) t.total += (double)hist[c];
+  t.code_b = text_code_bits(hist, &t.code_shift);
+  choose_tiling(n, t.tiling);
+  return t;
+}
+
 sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist, const uint32_t* order,
-                    uint32_t peel, int strategy, Plan& pl) {
+                    uint32_t peel, int strategy, Plan& pl, const TextInfo* tinfo = nullptr) {
   if (strategy < SM_STRATEGY_AUTO || strategy > SM_STRATEGY_PAIR) return fail(SM_EINVAL, "bad strategy");
+  TextInfo local;
+  if (!tinfo) {
+    local = text_info(hist, n);
+    tinfo = &local;
+  }
+  // PACKED applicability: the text's code field and every pattern symbol present in t
+  auto packed = [&]() -> int {
+    for (size_t j = 0; j < m; ++j)
+      if (hist[p[j]] == 0) return 0;  // an absent symbol: FILTER answers 0 at once
+    pl.code_shift = tinfo->code_shift;
+    return tinfo->code_b == 1 ? kPacked1 : (tinfo->code_b == 2 ? kPacked2 : 0);
+  };
   pl.order.resize(m);
   if (order) {
     if (!valid_permutation(order, m)) return fail(SM_EINVAL, "order is not a permutation of 0..m-1");
@@ -298,9 +330,9 @@ sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist
   } else {
     order_from_hist(hist, p, m, pl.order.data());
   }
-  choose_tiling(n, pl);
-  double total = 0;
-  for (int c = 0; c < 256; ++c) total += (double)hist[c];
+  pl.tile = tinfo->tiling.tile;
+  pl.cpl = tinfo->tiling.cpl;
+  const double total = tinfo->total;
   auto freq = [&](size_t k) { return total > 0 ? (double)hist[p[pl.order[k]]] / total : 0.0; };
   if (strategy == SM_STRATEGY_AUTO) {
     // Chunk-test hit rates (i.i.d. estimate from the histogram): FILTER queues the 16-byte
@@ -313,7 +345,7 @@ sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist
     if (h12 > tunables().block_min_hit) {
       strategy = kBlock;
       if (tunables().auto_packed) {  // small text alphabet: compare b-bit codes
-        const int pk = packed_projection(hist, p, m, &pl.code_shift);
+        const int pk = packed();
         if (pk) strategy = pk;
       }
     } else if (m >= 2 && h1 > tunables().pair_min_hit) {
@@ -324,7 +356,7 @@ sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist
   } else if (strategy == SM_STRATEGY_PAIR) {
     strategy = m >= 2 ? kPair : kFilter;
   } else if (strategy == SM_STRATEGY_PACKED) {
-    strategy = packed_projection(hist, p, m, &pl.code_shift);
+    strategy = packed();
     if (!strategy)
       return fail(SM_EINVAL, "SM_STRATEGY_PACKED needs <= 4 text symbols separable by a 1- or 2-bit field and "
                              "every pattern symbol present in the text");
@@ -561,6 +593,7 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
   if (pe != cudaSuccess) return cuda_fail(pe, "prepack");
   // plan and launch as we go: a batch is launched as soon as it is full, so the GPU
   // starts on the first patterns while the host still orders the later ones
+  const TextInfo tinfo = text_info(h, n);
   std::vector<Planned> plans(P);
   constexpr int kStrategies = 8;                  // index = strategy value (1..7)
   std::vector<const Planned*> batch[kStrategies];
@@ -578,7 +611,7 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
     if (n < ms[i] || lim == 0) continue;  // count stays 0
     Planned& q = plans[i];
     q = Planned{Plan(), ps[i], ms[i], d_counts + i};
-    sm_status s = make_plan(ps[i], ms[i], n, h, nullptr, 0, strategy, q.pl);
+    sm_status s = make_plan(ps[i], ms[i], n, h, nullptr, 0, strategy, q.pl, &tinfo);
     if (s != SM_OK) return s;
     use_codes(codes, cb, q.pl);
     const int k = q.pl.strategy;
@@ -637,12 +670,14 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
   cudaError_t pe = cudaSuccess;
   CodeArray codes{prepack_text(h, t, n, P, st, &cb, &pe), st};
   if (pe != cudaSuccess) return cuda_fail(pe, "prepack");
+  const TextInfo tinfo = text_info(h, n);
   std::vector<Planned> plans;
   plans.reserve(P);
   for (size_t i = 0; i < P; ++i) {
     if (n < ms[i] || lim == 0) continue;  // no alignments: count 0, no positions
     Planned q{Plan(), ps[i], ms[i], d_counts + i};
-    sm_status s = make_plan(ps[i], ms[i], n, h, P == 1 ? order : nullptr, P == 1 ? peel : 0, strategy, q.pl);
+    sm_status s = make_plan(ps[i], ms[i], n, h, P == 1 ? order : nullptr, P == 1 ? peel : 0, strategy, q.pl,
+                            &tinfo);
     if (s != SM_OK) return s;
     use_codes(codes, cb, q.pl);
     plans.push_back(std::move(q));
