@@ -919,10 +919,14 @@ __device__ __forceinline__ void stage_warp(const LaunchArgs& a, const PatDesc& d
 // = (pattern k, tile ti) in pattern-major order, round-robin over persistent CTAs
 // (one CTA flows from one pattern's last tiles into the next pattern's first).
 // ---------------------------------------------------------------------------
-// 3 CTAs per SM (2-stage rings of 32 KiB tiles); the reporting stage pass and the
-// pre-packed PACKED kernels are register-capped for 3 too
+// 3 CTAs per SM (2-stage rings of 32 KiB tiles): FILTER, PAIR and PACKED-PRE are
+// register-capped for 3 (BLOCK's Found4[CPL] registers would spill; per-tile PACKED is
+// held to 2 CTAs by its code buffers anyway; the overflow pass is rarely active)
 template <int STRAT, int EPI, int CAP, int CPL>
-__global__ void __launch_bounds__(kThreads, (is_prepacked(STRAT) || EPI == kEpiStage) ? 3 : 2)
+__global__ void __launch_bounds__(kThreads,
+                                  ((STRAT == kFilter || STRAT == kPair || is_prepacked(STRAT)) && EPI != kEpiWrite)
+                                      ? 3
+                                      : 2)
     search_kernel(const __grid_constant__ LaunchParams<CAP> P) {
   extern __shared__ __align__(128) uint8_t smem[];
   const LaunchArgs& a = P.a;
