@@ -61,6 +61,14 @@ def traffic_per_pass(config: str):
         return None
 
 
+def read_probe():
+    """Measured read-only streaming ceiling of the search kernel's TMA configuration (profiles/probe_r1.json)."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "profiles", "probe_r1.json")))["read_stream_GBps"])
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         d = json.load(open(MEASURED_PEAKS))
@@ -516,6 +524,8 @@ def run_native(args):
             "traffic_unit": "bytes per pattern pass (algorithmic n = %d)" % spec.n, "avg_launch_us": round(search_ms * 1e3 / P, 2),
             "kernel": "search_kernel (count)", "peak_kind": peak_kind,
             "algorithmic_bytes_per_launch": "n (text bytes of the launch's view)",
+            "read_stream_probe": read_probe(),
+            "frac_of_read_stream_probe": (round(achieved / read_probe(), 4) if read_probe() else None),
             "frac_note": "achieved counts the algorithmic n bytes of every pattern pass; the DRAM traffic per pass is "
                          "`traffic` (< n: alternating passes of a batch reuse the 126 MB L2) and the peak is the "
                          "measured COPY (read+write) rate, so frac can exceed 1 for a read-only stream",

@@ -21,8 +21,9 @@ if __name__ == "__main__":
         p = t.data_ptr()
         for bps in (2, 4, 8):
             res[f"ldg n={n>>20}MiB bps={bps}"] = round(lib.probe_ldg(p, n, bps, 10), 1)
-        for tile, stages, ctas, splits in [(32768, 3, 2, 1), (32768, 3, 2, 4), (16384, 6, 2, 1), (16384, 4, 3, 1),
-                                          (8192, 8, 3, 1), (65536, 3, 1, 1), (32768, 6, 1, 1), (16384, 12, 1, 1)]:
+        for tile, stages, ctas, splits in [(32768, 3, 2, 1), (32768, 2, 3, 1), (32768, 3, 2, 4), (16384, 6, 2, 1),
+                                          (16384, 4, 3, 1), (8192, 8, 3, 1), (65536, 3, 1, 1), (32768, 6, 1, 1),
+                                          (16384, 12, 1, 1)]:
             res[f"tma n={n>>20}MiB tile={tile} st={stages} ctas={ctas} split={splits}"] = round(
                 lib.probe_tma(p, n, tile, stages, ctas, splits, 8, 10), 1)
         del t
