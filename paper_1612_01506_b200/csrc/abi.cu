@@ -155,6 +155,7 @@ struct Tunables {
   double block_min_hit = 0.5;   // AUTO: BLOCK / PACKED when a pi(1)&pi(2) survivor is in > this share
   uint32_t l2_policy = 0;       // TMA load L2 policy: 0 evict_first, 1 evict_normal, 2 evict_last
   bool prepack = true;          // batches over <= 4-symbol texts: pack the text once (NEXT-3)
+  uint32_t prepack_min_p = 2;   // ... when the call has at least this many patterns
   int ctas_pre = 3;             // persistent CTAs per SM for the pre-packed PACKED kernels (small stages)
   uint32_t max_stages_pre = 6;  // their ring depth (3 CTAs x 6 stages of <= 9 KiB fit the SM)
 };
@@ -171,6 +172,7 @@ const Tunables& tunables() {
     if (const char* e = std::getenv("SMGPU_BLOCK_MIN_HIT")) x.block_min_hit = std::atof(e);
     if (const char* e = std::getenv("SMGPU_L2_POLICY")) x.l2_policy = (uint32_t)std::atoi(e) % 3u;
     if (const char* e = std::getenv("SMGPU_PREPACK")) x.prepack = std::atoi(e) != 0;
+    if (const char* e = std::getenv("SMGPU_PREPACK_MIN_P")) x.prepack_min_p = (uint32_t)std::atoi(e);
     if (const char* e = std::getenv("SMGPU_CTAS_PRE")) x.ctas_pre = std::atoi(e);
     if (x.ctas_pre < 1 || x.ctas_pre > 4) x.ctas_pre = 3;
     if (const char* e = std::getenv("SMGPU_STAGES_PRE")) x.max_stages_pre = (uint32_t)std::atoi(e);
@@ -253,7 +255,7 @@ uint8_t* prepack_text(const uint64_t* hist, const uint8_t* t, size_t n, size_t P
                       cudaError_t* err) {
   *err = cudaSuccess;
   *b_out = 0;
-  if (!tunables().prepack || P < 2 || n == 0) return nullptr;
+  if (!tunables().prepack || P < std::max<uint32_t>(1u, tunables().prepack_min_p) || n == 0) return nullptr;
   uint32_t shift = 0;
   const int b = text_code_bits(hist, &shift);
   if (!b) return nullptr;
