@@ -52,10 +52,24 @@ __device__ __forceinline__ void write_record(const uint8_t* rec, uint64_t out, u
     const uint32_t i = r0 + lane;
     uint32_t mk = i < words ? bm[i] : 0u;
     if (r0 + 32 <= words && __all_sync(0xFFFFFFFFu, mk == 0xFFFFFFFFu)) {
-      // every alignment of the round matches: positions are consecutive
-      const int64_t b0 = pos_base + (int64_t)(w * wspan + 32u * r0);
-      for (uint32_t q = lane; q < 1024u; q += 32)
-        if (o + q < cap) pos[o + q] = (uint64_t)(b0 + (int64_t)q);
+      // every alignment of the round matches: 1024 consecutive positions, written with
+      // 16-B stores (an odd head position first when pos + o is not 16-B aligned)
+      const uint64_t b0 = (uint64_t)(pos_base + (int64_t)(w * wspan + 32u * r0));
+      uint64_t* dst = pos + o;
+      if (o + 1024u <= cap) {
+        const uint32_t head = (uint32_t)((reinterpret_cast<uintptr_t>(dst) >> 3) & 1u);
+        if (head && lane == 0) dst[0] = b0;
+        ulonglong2* d2 = reinterpret_cast<ulonglong2*>(dst + head);
+        const uint32_t npairs = (1024u - head) / 2u;
+        for (uint32_t q = lane; q < npairs; q += 32) {
+          const unsigned long long v = b0 + head + 2u * q;
+          d2[q] = make_ulonglong2(v, v + 1);
+        }
+        if (((1024u - head) & 1u) && lane == 0) dst[1023] = b0 + 1023u;
+      } else {
+        for (uint32_t q = lane; q < 1024u; q += 32)
+          if (o + q < cap) dst[q] = b0 + q;
+      }
       o += 1024u;
       continue;
     }
