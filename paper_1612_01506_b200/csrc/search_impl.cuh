@@ -247,11 +247,23 @@ __device__ __forceinline__ bool chunk_hit(const uint4 v, uint32_t bc) {
 // (t[x + pi(1)] ^ p[pi(1)]) | (t[x + pi(2)] ^ p[pi(2)]) is zero iff alignment x matches
 // both, so one borrow-based zero-byte test on the OR covers the two comparisons
 // (exact as a whole-chunk predicate, like chunk_hit).  QA = word offset of pi(2)'s window.
-template <int QA>
+template <int QA, bool WORD_ALIGNED = false>
 __device__ __forceinline__ bool pair_hit(const uint8_t* buf, uint32_t c, uint32_t pre, uint32_t s2, uint32_t bc1,
                                          uint32_t bc2) {
   const uint4 v1 = lds128(buf + pre + 16u * c);
-  const uint4 v2 = window16_q<QA>(buf + 16u * c + (s2 & ~15u), (s2 & 3u) * 8u);
+  uint4 v2;
+  if constexpr (WORD_ALIGNED) {  // pi(2)'s window starts on a word: no funnel shifts
+    if constexpr (QA == 0) {
+      v2 = lds128(buf + 16u * c + (s2 & ~15u));
+    } else {
+      const uint4 lo = lds128(buf + 16u * c + (s2 & ~15u));
+      const uint4 hi = lds128(buf + 16u * c + (s2 & ~15u) + 16u);
+      const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+      v2 = make_uint4(w[QA], w[QA + 1], w[QA + 2], w[QA + 3]);
+    }
+  } else {
+    v2 = window16_q<QA>(buf + 16u * c + (s2 & ~15u), (s2 & 3u) * 8u);
+  }
   const uint32_t y0 = (v1.x ^ bc1) | (v2.x ^ bc2), y1 = (v1.y ^ bc1) | (v2.y ^ bc2);
   const uint32_t y2 = (v1.z ^ bc1) | (v2.z ^ bc2), y3 = (v1.w ^ bc1) | (v2.w ^ bc2);
   return ((((y0 - 0x01010101u) & ~y0) | ((y1 - 0x01010101u) & ~y1) | ((y2 - 0x01010101u) & ~y2) |
@@ -429,8 +441,9 @@ __device__ __forceinline__ void filter_drain(const Pat& pt, const uint8_t* buf, 
 // ballot-compacts the chunks whose pi(1)-bytes contain p[pi(1)] into the warp's
 // queue (ascending chunk order); phase B (filter_drain) verifies them.
 // PA (PAIR strategy): phase A tests pi(1) and pi(2) together (pair_hit, pi(2)'s window
-// class QA), so only chunks with a pi(1)&pi(2) survivor are queued -- for frequent pi(1).
-template <int CPL, bool PA, int QA, class Sink>
+// class QA; WA: the window is word-aligned), so only chunks with a pi(1)&pi(2) survivor
+// are queued -- for frequent pi(1).
+template <int CPL, bool PA, int QA, class Sink, bool WA = false>
 __device__ __forceinline__ void filter_tile_q(const Pat& pt, const uint8_t* buf, uint32_t cw0, int lane, uint16_t* qc,
                                               bool edge, int32_t rlo, int32_t rhi, Sink& sink, Ctr& C) {
   C.add(kCtrChunks, 32u * CPL);
@@ -443,7 +456,7 @@ __device__ __forceinline__ void filter_tile_q(const Pat& pt, const uint8_t* buf,
       const uint32_t c = cw0 + it * 32u + lane;
       SMGPU_DCHECK(pt.pre + 16u * c + 16u <= pt.lim);
       bool hit;
-      if constexpr (PA) hit = pair_hit<QA>(buf, c, pt.pre, pt.s2, pt.bc1, pt.bc2);
+      if constexpr (PA) hit = pair_hit<QA, WA>(buf, c, pt.pre, pt.s2, pt.bc1, pt.bc2);
       else hit = chunk_hit(lds128(buf + pt.pre + 16u * c), pt.bc1);
       const uint32_t bal = __ballot_sync(0xFFFFFFFFu, hit);
       if (hit) qc[qlen + __popc(bal & lanemask_lt())] = (uint16_t)c;
@@ -470,11 +483,24 @@ __device__ __forceinline__ void filter_tile(const Pat& pt, const uint8_t* buf, u
 template <int CPL, class Sink>
 __device__ __forceinline__ void pair_tile(const Pat& pt, const uint8_t* buf, uint32_t cw0, int lane, uint16_t* qc,
                                           bool edge, int32_t rlo, int32_t rhi, Sink& sink, Ctr& C) {
+  const bool wa = (pt.s2 & 3u) == 0;  // warp-uniform
   switch ((pt.s2 >> 2) & 3u) {  // warp-uniform
-    case 0: filter_tile_q<CPL, true, 0>(pt, buf, cw0, lane, qc, edge, rlo, rhi, sink, C); break;
-    case 1: filter_tile_q<CPL, true, 1>(pt, buf, cw0, lane, qc, edge, rlo, rhi, sink, C); break;
-    case 2: filter_tile_q<CPL, true, 2>(pt, buf, cw0, lane, qc, edge, rlo, rhi, sink, C); break;
-    default: filter_tile_q<CPL, true, 3>(pt, buf, cw0, lane, qc, edge, rlo, rhi, sink, C); break;
+    case 0:
+      if (wa) filter_tile_q<CPL, true, 0, Sink, true>(pt, buf, cw0, lane, qc, edge, rlo, rhi, sink, C);
+      else filter_tile_q<CPL, true, 0>(pt, buf, cw0, lane, qc, edge, rlo, rhi, sink, C);
+      break;
+    case 1:
+      if (wa) filter_tile_q<CPL, true, 1, Sink, true>(pt, buf, cw0, lane, qc, edge, rlo, rhi, sink, C);
+      else filter_tile_q<CPL, true, 1>(pt, buf, cw0, lane, qc, edge, rlo, rhi, sink, C);
+      break;
+    case 2:
+      if (wa) filter_tile_q<CPL, true, 2, Sink, true>(pt, buf, cw0, lane, qc, edge, rlo, rhi, sink, C);
+      else filter_tile_q<CPL, true, 2>(pt, buf, cw0, lane, qc, edge, rlo, rhi, sink, C);
+      break;
+    default:
+      if (wa) filter_tile_q<CPL, true, 3, Sink, true>(pt, buf, cw0, lane, qc, edge, rlo, rhi, sink, C);
+      else filter_tile_q<CPL, true, 3>(pt, buf, cw0, lane, qc, edge, rlo, rhi, sink, C);
+      break;
   }
 }
 
