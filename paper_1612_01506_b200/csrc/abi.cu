@@ -156,6 +156,7 @@ struct Tunables {
   uint32_t l2_policy = 0;       // TMA load L2 policy: 0 evict_first, 1 evict_normal, 2 evict_last
   bool prepack = true;          // batches over <= 4-symbol texts: pack the text once (NEXT-3)
   uint32_t prepack_min_p = 2;   // ... when the call has at least this many patterns
+  double pair_align_slack = 6;  // PAIR: prefer a word-aligned pi(2) within this frequency factor (<= 1: off)
   int ctas_pre = 3;             // persistent CTAs per SM for the pre-packed PACKED kernels (small stages)
   uint32_t max_stages_pre = 6;  // their ring depth (3 CTAs x 6 stages of <= 9 KiB fit the SM)
 };
@@ -173,6 +174,7 @@ const Tunables& tunables() {
     if (const char* e = std::getenv("SMGPU_L2_POLICY")) x.l2_policy = (uint32_t)std::atoi(e) % 3u;
     if (const char* e = std::getenv("SMGPU_PREPACK")) x.prepack = std::atoi(e) != 0;
     if (const char* e = std::getenv("SMGPU_PREPACK_MIN_P")) x.prepack_min_p = (uint32_t)std::atoi(e);
+    if (const char* e = std::getenv("SMGPU_PAIR_ALIGN")) x.pair_align_slack = std::atof(e);
     if (const char* e = std::getenv("SMGPU_CTAS_PRE")) x.ctas_pre = std::atoi(e);
     if (x.ctas_pre < 1 || x.ctas_pre > 4) x.ctas_pre = 3;
     if (const char* e = std::getenv("SMGPU_STAGES_PRE")) x.max_stages_pre = (uint32_t)std::atoi(e);
@@ -375,7 +377,24 @@ sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist
   }
   pl.r = std::min<uint32_t>(peel, (uint32_t)m);
   if (pl.strategy == kFilter) pl.r = 1;
-  if (pl.strategy == kPair) pl.r = 2;  // pi(1), pi(2) tested together
+  if (pl.strategy == kPair) {
+    pl.r = 2;  // pi(1), pi(2) tested together
+    // PAIR's chunk test is cheaper when pi(2)'s window is word-aligned relative to
+    // pi(1)'s ((a2 - a1) % 4 == 0: no funnel shifts); among the next positions whose
+    // symbol is at most pair_align_slack times as frequent as pi(2)'s, move the first
+    // aligned one to pi(2).  The comparison order never changes the result.
+    const double slack = tunables().pair_align_slack;
+    if (slack > 1.0 && !order && m >= 3) {
+      const uint32_t a1 = pl.order[0];
+      const double f2 = (double)hist[p[pl.order[1]]];
+      for (size_t k = 1; k < m && (double)hist[p[pl.order[k]]] <= slack * f2; ++k) {
+        if (((pl.order[k] - a1) & 3u) == 0) {
+          std::swap(pl.order[1], pl.order[k]);
+          break;
+        }
+      }
+    }
+  }
   return SM_OK;
 }
 
