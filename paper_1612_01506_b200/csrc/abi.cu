@@ -157,6 +157,7 @@ struct Tunables {
   bool prepack = true;          // batches over <= 4-symbol texts: pack the text once (NEXT-3)
   uint32_t prepack_min_p = 2;   // ... when the call has at least this many patterns
   double pair_align_slack = 6;  // PAIR: prefer a word-aligned pi(2) within this frequency factor (<= 1: off)
+  int peel_bias = 0;            // added to the AUTO peeling factor (tuning; +2 measured slower)
   int ctas_pre = 3;             // persistent CTAs per SM for the pre-packed PACKED kernels (small stages)
   uint32_t max_stages_pre = 6;  // their ring depth (3 CTAs x 6 stages of <= 9 KiB fit the SM)
 };
@@ -175,6 +176,7 @@ const Tunables& tunables() {
     if (const char* e = std::getenv("SMGPU_PREPACK")) x.prepack = std::atoi(e) != 0;
     if (const char* e = std::getenv("SMGPU_PREPACK_MIN_P")) x.prepack_min_p = (uint32_t)std::atoi(e);
     if (const char* e = std::getenv("SMGPU_PAIR_ALIGN")) x.pair_align_slack = std::atof(e);
+    if (const char* e = std::getenv("SMGPU_PEEL_BIAS")) x.peel_bias = std::atoi(e);
     if (const char* e = std::getenv("SMGPU_CTAS_PRE")) x.ctas_pre = std::atoi(e);
     if (x.ctas_pre < 1 || x.ctas_pre > 4) x.ctas_pre = 3;
     if (const char* e = std::getenv("SMGPU_STAGES_PRE")) x.max_stages_pre = (uint32_t)std::atoi(e);
@@ -373,7 +375,8 @@ sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist
     double surv = std::min(32.0 * 16.0 * pl.cpl, 2048.0);
     uint32_t r = 0;
     while (r < m && surv > 0.5) surv *= freq(r++);
-    peel = r < 1 ? 1 : r;
+    const int rb = (int)r + tunables().peel_bias;  // tuning knob (0 by default)
+    peel = rb < 1 ? 1u : (uint32_t)rb;
   }
   pl.r = std::min<uint32_t>(peel, (uint32_t)m);
   if (pl.strategy == kFilter) pl.r = 1;
