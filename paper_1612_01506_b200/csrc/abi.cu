@@ -152,6 +152,7 @@ struct Tunables {
   bool auto_packed = true;      // AUTO may pick PACKED for small text alphabets
   bool alternate = true;        // batches: odd patterns scan the text backwards (L2 reuse at the seam)
   double pair_min_hit = 0.2;    // AUTO: PAIR instead of FILTER when p[pi(1)] is in > this share of 16-B chunks
+  double pair_min_hit_long = 0.12;  // ... for m >= 32 (a word-aligned pi(2) is then almost always available)
   double block_min_hit = 0.5;   // AUTO: BLOCK / PACKED when a pi(1)&pi(2) survivor is in > this share
   uint32_t l2_policy = 0;       // TMA load L2 policy: 0 evict_first, 1 evict_normal, 2 evict_last
   bool prepack = true;          // batches over <= 4-symbol texts: pack the text once (NEXT-3)
@@ -171,6 +172,7 @@ const Tunables& tunables() {
     if (const char* e = std::getenv("SMGPU_AUTO_PACKED")) x.auto_packed = std::atoi(e) != 0;
     if (const char* e = std::getenv("SMGPU_ALTERNATE")) x.alternate = std::atoi(e) != 0;
     if (const char* e = std::getenv("SMGPU_PAIR_MIN_HIT")) x.pair_min_hit = std::atof(e);
+    if (const char* e = std::getenv("SMGPU_PAIR_MIN_HIT_LONG")) x.pair_min_hit_long = std::atof(e);
     if (const char* e = std::getenv("SMGPU_BLOCK_MIN_HIT")) x.block_min_hit = std::atof(e);
     if (const char* e = std::getenv("SMGPU_L2_POLICY")) x.l2_policy = (uint32_t)std::atoi(e) % 3u;
     if (const char* e = std::getenv("SMGPU_PREPACK")) x.prepack = std::atoi(e) != 0;
@@ -354,7 +356,7 @@ sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist
         const int pk = packed();
         if (pk) strategy = pk;
       }
-    } else if (m >= 2 && h1 > tunables().pair_min_hit) {
+    } else if (m >= 2 && h1 > (m >= 32 ? tunables().pair_min_hit_long : tunables().pair_min_hit)) {
       strategy = kPair;
     } else {
       strategy = kFilter;

@@ -66,7 +66,7 @@ def test_plan_policy(sm):
 def test_plan_auto_rule(sm):
     """AUTO (abi.cu make_plan, profiles/strategy_pair_r1.md): h1 = 1-(1-f1)^16 is FILTER's chunk
     queue rate, h12 = 1-(1-f1 f2)^16 PAIR's (h1 for m = 1); BLOCK/PACKED if h12 > 0.5, else PAIR
-    if m >= 2 and h1 > 0.2, else FILTER."""
+    if m >= 2 and h1 > 0.2 (0.12 for m >= 32), else FILTER."""
     h = np.zeros(256, dtype=np.uint64)
     # 20 symbols 'A'..'T': two frequent (10 % each), the rest rare
     for i, c in enumerate(range(65, 85)):
