@@ -159,6 +159,7 @@ struct Tunables {
   uint32_t prepack_min_p = 2;   // ... when the call has at least this many patterns
   double pair_align_slack = 6;  // PAIR: prefer a word-aligned pi(2) within this frequency factor (<= 1: off)
   int peel_bias = 0;            // added to the AUTO peeling factor (tuning; +2 measured slower)
+  uint32_t wait_ns = 0;         // consumers' stage wait: suspend-time hint in ns (0 = spin)
   int ctas_pre = 3;             // persistent CTAs per SM for the pre-packed PACKED kernels (small stages)
   uint32_t max_stages_pre = 6;  // their ring depth (3 CTAs x 6 stages of <= 9 KiB fit the SM)
 };
@@ -179,6 +180,7 @@ const Tunables& tunables() {
     if (const char* e = std::getenv("SMGPU_PREPACK_MIN_P")) x.prepack_min_p = (uint32_t)std::atoi(e);
     if (const char* e = std::getenv("SMGPU_PAIR_ALIGN")) x.pair_align_slack = std::atof(e);
     if (const char* e = std::getenv("SMGPU_PEEL_BIAS")) x.peel_bias = std::atoi(e);
+    if (const char* e = std::getenv("SMGPU_WAIT_NS")) x.wait_ns = (uint32_t)std::atoi(e);
     if (const char* e = std::getenv("SMGPU_CTAS_PRE")) x.ctas_pre = std::atoi(e);
     if (x.ctas_pre < 1 || x.ctas_pre > 4) x.ctas_pre = 3;
     if (const char* e = std::getenv("SMGPU_STAGES_PRE")) x.max_stages_pre = (uint32_t)std::atoi(e);
@@ -497,6 +499,7 @@ void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_
   L.a.tbl_words = (uint32_t)L.e.size();
   L.a.ctr = counters_ptr();
   L.a.l2_policy = tunables().l2_policy;
+  L.a.wait_ns = tunables().wait_ns;
   // reporting launches reserve the per-warp position lists
   L.a.list_off = (kTblOff + 127) & ~127u;
   // reporting: kEpiStage keeps one 32 CPL-mask bitmap per warp (<= 512 B), the overflow

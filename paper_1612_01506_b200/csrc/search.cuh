@@ -96,6 +96,7 @@ struct LaunchArgs {
   uint32_t tbl_words;        // table entries
   uint32_t code_shift;       // PACKED: code(x) = (x >> code_shift) & (2^b - 1), injective on the text's symbols
   uint32_t l2_policy;        // TMA loads: 0 evict_first, 1 evict_normal, 2 evict_last (performance only)
+  uint32_t wait_ns;          // consumers' full-stage wait: suspend-time hint (0 = spin)
   uint32_t pack_off;         // PACKED: smem byte offset of the double-buffered code array
   uint32_t pack_bytes;       // PACKED: bytes of one code buffer
   const uint8_t* codes;      // kPackedBPre: the code array of the text (base-relative alignment x <-> code bits

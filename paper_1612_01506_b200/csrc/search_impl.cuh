@@ -1007,7 +1007,8 @@ __global__ void __launch_bounds__(kThreads,
     }
     const PatDesc& d = P.d[k];
     const uint64_t item = d.item_base + ti;
-    mbar_wait(&full[s], ph);
+    if (a.wait_ns) mbar_wait_sleep(&full[s], ph, a.wait_ns);
+    else mbar_wait(&full[s], ph);
     const uint8_t* buf = ring + (size_t)s * a.stage_stride;
     const Pat pt{d.m, d.r, d.a1, d.bc1, d.s2, d.bc2, d.pre, (d.flags >> 8) & 0xFFu, d.stage_len, P.e + d.tbl};
     const bool edge = ti < d.edge_lo || ti >= d.edge_hi;  // tile holds invalid alignments
