@@ -251,25 +251,30 @@ def dense_report(sm, synth, dev, stream, peak, reps: int = 3):
     pos = torch.empty(total, dtype=torch.int64, device=dev)
     d = torch.zeros(1, dtype=torch.int64, device=dev)
     pb = sm.PatternBatch([b"a" * m])
-    sm.sm_report_batch(pb, t, pos, d)
+    # A1 once per text (timed separately, amortised over the patterns)
+    hist = sm.sm_histogram(t)
+    sm.sm_report_batch(pb, t, pos, d, hist=hist)
     torch.cuda.synchronize()
     assert int(d.item()) == total
     assert int(pos[-1].item()) == total - 1 and int(pos[12345].item()) == 12345
-    ms = []
+    ms, hist_ms = [], []
     for _ in range(reps):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record(stream)
-        sm.sm_report_batch(pb, t, pos, d)
+        hist = sm.sm_histogram(t)
         e1.record(stream)
+        sm.sm_report_batch(pb, t, pos, d, hist=hist)
+        e2.record(stream)
         torch.cuda.synchronize()
-        ms.append(e0.elapsed_time(e1))
+        hist_ms.append(e0.elapsed_time(e1))
+        ms.append(e1.elapsed_time(e2))
     best = min(ms)
     moved = spec.n + 8 * total
     gbs = moved / (best * 1e-3) / 1e9
     del pos, t
     torch.cuda.empty_cache()
     return {"workload": "c4p periodic a^(2^30), p = a^17 (every alignment matches)", "positions": total,
-            "ms": round(best, 3), "bytes_moved": moved, "GBps": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4),
+            "ms": round(best, 3), "histogram_ms": round(min(hist_ms), 3), "bytes_moved": moved, "GBps": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4),
             "text_GBps": round(spec.n / (best * 1e-3) / 1e9, 1)}
 
 

@@ -867,7 +867,7 @@ struct StageAlloc {
 };
 
 // Reporting pass 1, one warp with wcnt > 0 matches in work item `item`: post its count
-// (wc, per-pattern total), then write its record -- the ascending u16 list of
+// (wc; the per-pattern total is accumulated by the caller like a count), then write its record -- the ascending u16 list of
 // tile-relative alignments when sparse, its bitmap when dense -- followed by a zero
 // terminator header.  No other warp is waited for.  If the pool is exhausted the item
 // is queued (once) for the overflow pass, which recomputes it from the text.
@@ -879,8 +879,7 @@ __device__ __forceinline__ void stage_warp(const LaunchArgs& a, const PatDesc& d
   const uint32_t dbytes = rec_warp_bytes(wcnt, kWspan);
   unsigned long long o = 0;
   if (lane == 0) {
-    a.wc[item * kConsumerWarps + warp] = (uint16_t)wcnt;
-    atomicAdd(reinterpret_cast<unsigned long long*>(d.count_out), (unsigned long long)wcnt);
+    a.wc[item * kConsumerWarps + warp] = (uint16_t)wcnt;  // (the pattern total: the caller's acc)
     o = al.take(a, 1u + dbytes / 16u);
     if (o == ~0ull && !(atomicOr(&a.ovf_bits[item >> 5], 1u << (item & 31)) & (1u << (item & 31))))
       a.ovf_items[atomicAdd(a.ovf_n, 1u)] = (uint32_t)item;
@@ -988,8 +987,8 @@ __global__ void __launch_bounds__(kThreads,
   const uint32_t T = a.tile;
   const uint32_t cw0 = (uint32_t)warp * 32u * CPL;  // first chunk of this warp
   uint32_t s = 0, ph = 0, par = 0, par_pk = 0;
-  uint32_t kc = 0;   // kEpiCount: pattern whose matches `acc` holds
-  uint32_t acc = 0;  // kEpiCount: this lane's matches of pattern kc so far
+  uint32_t kc = 0;   // count / stage: pattern whose matches `acc` holds
+  uint32_t acc = 0;  // count / stage: this lane's matches of pattern kc so far
   Ctr C;
 #ifdef SMGPU_COUNTERS
   C.v[kCtrAlphaEff] = (STRAT == kFilter || STRAT == kPair) ? 0ull : 512ull * CPL;
@@ -999,7 +998,7 @@ __global__ void __launch_bounds__(kThreads,
   uint64_t ti;
   while (items.advance(P, k, ti)) {
     C.add(kCtrWarpTiles, 1);
-    if (EPI == kEpiCount && k != kc) {  // flush pattern kc (warp-uniform; k only grows here)
+    if (EPI != kEpiWrite && k != kc) {  // flush pattern kc (warp-uniform; k only grows here)
       const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, acc);
       if (lane == 0 && ws) count_add(a, P.d[kc].count_out, ws);
       acc = 0;
@@ -1038,6 +1037,7 @@ __global__ void __launch_bounds__(kThreads,
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         released = true;
+        acc += sk.n;
         const uint32_t wcnt = __reduce_add_sync(0xFFFFFFFFu, sk.n);
         if (wcnt) stage_warp<CPL, true>(a, d, list, salloc, warp, lane, item, pos_base, wcnt);
       } else {  // overflow pass: buffer this warp's matches, exchange warp totals, write coalesced
@@ -1073,6 +1073,7 @@ __global__ void __launch_bounds__(kThreads,
         acc += tc;
       } else if (EPI == kEpiStage) {
         constexpr bool kWide = B == 1 && CPL >= 2;  // 32-bit masks of 32 alignments
+        acc += tc;
         const uint32_t wcnt = __reduce_add_sync(0xFFFFFFFFu, tc);
         if (wcnt) {
 #pragma unroll
@@ -1101,6 +1102,7 @@ __global__ void __launch_bounds__(kThreads,
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         released = true;
+        acc += tc;
         const uint32_t wcnt = __reduce_add_sync(0xFFFFFFFFu, tc);
         if (wcnt) {
 #pragma unroll
@@ -1122,7 +1124,7 @@ __global__ void __launch_bounds__(kThreads,
     }
   }
 
-  if (EPI == kEpiCount) {
+  if (EPI != kEpiWrite) {
     const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, acc);
     if (lane == 0 && ws) count_add(a, P.d[kc].count_out, ws);
   }
