@@ -162,6 +162,8 @@ struct Tunables {
   uint32_t wait_ns = 0;         // consumers' stage wait: suspend-time hint in ns (0 = spin)
   int ctas_pre = 3;             // persistent CTAs per SM for the pre-packed PACKED kernels (small stages)
   uint32_t max_stages_pre = 6;  // their ring depth (3 CTAs x 6 stages of <= 9 KiB fit the SM)
+  bool dispatch = true;         // batch calls: work items fetched from a counter (search.cuh work_ctr)
+  uint64_t dispatch_min_bytes = 64ull << 20;  // ... when the call streams at least this much text (n x P)
 };
 
 const Tunables& tunables() {
@@ -182,6 +184,8 @@ const Tunables& tunables() {
     if (const char* e = std::getenv("SMGPU_PEEL_BIAS")) x.peel_bias = std::atoi(e);
     if (const char* e = std::getenv("SMGPU_WAIT_NS")) x.wait_ns = (uint32_t)std::atoi(e);
     if (const char* e = std::getenv("SMGPU_CTAS_PRE")) x.ctas_pre = std::atoi(e);
+    if (const char* e = std::getenv("SMGPU_DISPATCH")) x.dispatch = std::atoi(e) != 0;
+    if (const char* e = std::getenv("SMGPU_DISPATCH_MIN_MB")) x.dispatch_min_bytes = (uint64_t)std::atoll(e) << 20;
     if (x.ctas_pre < 1 || x.ctas_pre > 4) x.ctas_pre = 3;
     if (const char* e = std::getenv("SMGPU_STAGES_PRE")) x.max_stages_pre = (uint32_t)std::atoi(e);
     if (x.max_stages_pre < 2 || x.max_stages_pre > (uint32_t)kMaxStages) x.max_stages_pre = 6;
@@ -623,6 +627,27 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
   // plan and launch as we go: a batch is launched as soon as it is full, so the GPU
   // starts on the first patterns while the host still orders the later ones
   const TextInfo tinfo = text_info(h, n);
+  // counter-dispatched work items for long calls: one zeroed counter per launch
+  // (a call makes at most P + 7 launches: every flush holds >= 1 pattern)
+  unsigned long long* work = nullptr;
+  size_t nwork = 0, used_work = 0;
+  if (tunables().dispatch && (uint64_t)n * P >= tunables().dispatch_min_bytes) {
+    keep_pool_cached();
+    nwork = P + 8;
+    SM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&work), nwork * 8, st), "cudaMallocAsync(work counters)");
+    cudaError_t e = cudaMemsetAsync(work, 0, nwork * 8, st);
+    if (e != cudaSuccess) {
+      cudaFreeAsync(work, st);
+      return cuda_fail(e, "cudaMemsetAsync(work counters)");
+    }
+  }
+  struct FreeWork {
+    unsigned long long* p;
+    cudaStream_t st;
+    ~FreeWork() {
+      if (p) cudaFreeAsync(p, st);
+    }
+  } free_work{work, st};
   std::vector<Planned> plans(P);
   constexpr int kStrategies = 8;                  // index = strategy value (1..7)
   std::vector<const Planned*> batch[kStrategies];
@@ -632,6 +657,7 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
     HostLaunch L;
     build_launch(batch[strat], t, n, lim, kEpiCount, L);
     L.a.codes = codes.p;
+    if (work && used_work < nwork && L.a.total_work < kNoItem) L.a.work_ctr = work + used_work++;
     batch[strat].clear();
     words[strat] = 0;
     return launch_checked(L, st, "search kernel (batch)");
@@ -763,7 +789,7 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
   auto al = [](uint64_t b) { return (b + 255) & ~255ull; };
   const uint64_t nL = Ls.size();
   const uint64_t wc_b = al(items * 16), offs_b = al(items * 8), bits_b = al((items + 31) / 32 * 4),
-                 ovf_b = al(items * 4), ctr_b = al(8 + nL * 4), temp_b = al(temp_bytes),
+                 ovf_b = al(items * 4), ctr_b = al(16 + nL * 12), temp_b = al(temp_bytes),
                  stage_b = stage_pool_bytes(cap);
   uint8_t* scratch = nullptr;
   SM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&scratch),
@@ -773,7 +799,10 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
   uint16_t* wc = reinterpret_cast<uint16_t*>(q); q += wc_b;
   uint32_t* ovf_bits = reinterpret_cast<uint32_t*>(q); q += bits_b;
   unsigned long long* stage_used = reinterpret_cast<unsigned long long*>(q);
-  uint32_t* ovf_n = reinterpret_cast<uint32_t*>(q + 8); q += ctr_b;
+  unsigned long long* expand_work = stage_used + 1;
+  unsigned long long* work = reinterpret_cast<unsigned long long*>(q + 16);  // [nL] pass-1 dispatch counters
+  uint32_t* ovf_n = reinterpret_cast<uint32_t*>(q + 16 + nL * 8); q += ctr_b;
+  const bool dispatch = tunables().dispatch && (uint64_t)n * P >= tunables().dispatch_min_bytes;
   uint64_t* offsets = reinterpret_cast<uint64_t*>(q); q += offs_b;
   uint32_t* ovf_items = reinterpret_cast<uint32_t*>(q); q += ovf_b;
   void* temp = q; q += temp_b;
@@ -791,6 +820,7 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
     L.a.ovf_items = ovf_items + ovf_at;  // this launch's overflow queue (capacity: its items)
     L.a.ovf_n = ovf_n + li;
     L.a.pos_offset = pos_offset;
+    if (dispatch && L.a.total_work < kNoItem) L.a.work_ctr = work + li;
     ovf_at += L.a.total_work;
     e = launch_search(L, st);
     if (e == cudaSuccess) ++g_launches;
@@ -800,7 +830,7 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
     if (e == cudaSuccess) g_launches += 1;
   }
   if (e == cudaSuccess) {
-    e = launch_stage_expand(stage, stage_used, stage_b / 16, wc, offsets, pos, cap, num_sms(), st);
+    e = launch_stage_expand(stage, stage_used, stage_b / 16, wc, offsets, pos, cap, expand_work, num_sms(), st);
     if (e == cudaSuccess) ++g_launches;
   }
   for (size_t li = 0; li < Ls.size(); ++li) {  // overflow pass (CTAs exit at once when the queue is empty)

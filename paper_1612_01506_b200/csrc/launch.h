@@ -31,7 +31,7 @@ cudaError_t launch_search(const HostLaunch& L, cudaStream_t stream);
 // see search.cuh.
 cudaError_t launch_stage_expand(const uint8_t* stage, const unsigned long long* stage_used, uint64_t stage_cap16,
                                 const uint16_t* wc, const uint64_t* tile_offsets, uint64_t* pos, uint64_t cap,
-                                int num_sms, cudaStream_t st);
+                                unsigned long long* work /* zeroed chunk counter */, int num_sms, cudaStream_t st);
 
 // NEXT-3: the text's b-bit code array (code(x) = (x >> shift) & (2^b - 1)), base-relative
 // alignment x <-> bits [b x, b x + b); code_bytes (multiple of 16) of it, zero past the text

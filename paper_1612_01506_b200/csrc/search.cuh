@@ -19,10 +19,12 @@ constexpr int kTableLarge = 6400;                        // with 64 descriptors:
 constexpr int kBatchTableWords = kTableLarge;            // batching: table entries per launch
 
 // shared-memory layout: [full/empty mbarriers][warp totals [2][W]][queue chunk ids u16 [W][kQueueLen]]
-//                       [PACKED code buffers][ring]   (the pattern tables stay in the kernel parameters)
+//                       [dispatched item per stage u32][PACKED code buffers][ring]   (the pattern tables stay in the kernel parameters)
 constexpr uint32_t kWarpTotOff = 2 * kMaxStages * 8;
 constexpr uint32_t kQueueOff = kWarpTotOff + 2 * kConsumerWarps * 4;
-constexpr uint32_t kTblOff = kQueueOff + kConsumerWarps * kQueueLen * 2;  // end of the fixed region
+constexpr uint32_t kTixOff = kQueueOff + kConsumerWarps * kQueueLen * 2;  // [kMaxStages] u32 dispatched items
+constexpr uint32_t kTblOff = kTixOff + kMaxStages * 4;                      // end of the fixed region
+constexpr uint32_t kNoItem = 0xFFFFFFFFu;  // dispatched-item sentinel: the producer is done
 
 // kPackedB: b-bit codes; kPair: FILTER whose chunk test covers pi(1) and pi(2) together
 // kPackedBPre: PACKED reading a code array packed once per call (pack_text_kernel) instead
@@ -114,6 +116,8 @@ struct LaunchArgs {
   uint64_t cap;              // kEpiWrite: capacity of pos
   uint64_t pos_offset;       // kEpiStage / kEpiWrite: added to every position (a shard's first owned position)
   unsigned long long* ctr;   // instrumented build (SMGPU_COUNTERS) only: device u64[kCounters], else unused
+  unsigned long long* work_ctr;  // count / stage: non-null = work items are dispatched from this zeroed
+                                 // counter (the producer fetches, the consumers read the stage's item)
 };
 
 // Compare-step counters of the instrumented build (libsmgpu_counters.so, NEXT-2):

@@ -152,6 +152,13 @@ struct WorkIter {
   uint32_t k = 0;
   __device__ __forceinline__ explicit WorkIter(const LaunchParams<CAP>& P)
       : end(EPI == kEpiWrite ? (uint64_t)*P.a.ovf_n : P.a.total_work) {}
+  // (pattern, tile) of pattern-major work index w; w must not decrease between calls
+  __device__ __forceinline__ void map(const LaunchParams<CAP>& P, uint64_t w, uint32_t& kk, uint64_t& ti) {
+    while (w >= P.d[k].work_end) ++k;
+    kk = k;
+    ti = w - (P.d[k].work_end - P.d[k].ntiles);
+    if (P.d[k].flags & 1u) ti = P.d[k].ntiles - 1 - ti;  // alternating scan direction
+  }
   __device__ __forceinline__ bool advance(const LaunchParams<CAP>& P, uint32_t& kk, uint64_t& ti) {
     if (next >= end) return false;
     if (EPI == kEpiWrite) {
@@ -162,10 +169,7 @@ struct WorkIter {
       kk = j;
       ti = item - P.d[j].item_base;
     } else {
-      while (next >= P.d[k].work_end) ++k;
-      kk = k;
-      ti = next - (P.d[k].work_end - P.d[k].ntiles);
-      if (P.d[k].flags & 1u) ti = P.d[k].ntiles - 1 - ti;  // alternating scan direction
+      map(P, next, kk, ti);
     }
     next += gridDim.x;
     return true;
@@ -178,8 +182,14 @@ struct WorkIter {
 // cp.async.bulk for the aligned interior, completion counted on full[s].
 // ---------------------------------------------------------------------------
 // PRE: kPackedBPre -- tiles come from the code array (CB code bits per alignment).
+// Work dispatch: statically round-robin (item = blockIdx.x + j gridDim.x), or, with
+// a.work_ctr, fetched from a counter in the order CTAs become free -- which keeps the
+// window of text being read at any moment narrow (TMA ring probe on 4 GiB: 7.48-7.51 vs
+// 7.21-7.26 TB/s static, tools/probe_dyn.py).  The producer fetches and publishes the
+// item in tix[stage] before arming the stage; consumers read it after the stage's wait.
 template <int EPI, int CAP, bool PRE = false, int CB = 1>
-__device__ void produce(const LaunchParams<CAP>& P, uint8_t* ring, uint64_t* full, uint64_t* empty) {
+__device__ void produce(const LaunchParams<CAP>& P, uint8_t* ring, uint64_t* full, uint64_t* empty,
+                        uint32_t* tix) {
   const LaunchArgs& a = P.a;
   const uint64_t pol = a.l2_policy == 2 ? l2_policy_evict_last()
                        : a.l2_policy == 1 ? l2_policy_evict_normal() : l2_policy_evict_first();
@@ -187,11 +197,21 @@ __device__ void produce(const LaunchParams<CAP>& P, uint8_t* ring, uint64_t* ful
   uint32_t s = 0, ph = 0;  // stage and its use parity
   bool wrapped = false;
   WorkIter<EPI, CAP> items(P);
+  const bool dyn = EPI != kEpiWrite && a.work_ctr != nullptr;
   uint32_t k;
   uint64_t ti;
-  while (items.advance(P, k, ti)) {
+  while (true) {
+    uint64_t w = 0;
+    if (dyn) {
+      w = atomicAdd(a.work_ctr, 1ull);
+      if (w >= a.total_work) break;
+      items.map(P, w, k, ti);
+    } else if (!items.advance(P, k, ti)) {
+      break;
+    }
     const PatDesc& d = P.d[k];
     if (wrapped) mbar_wait_sleep(&empty[s], ph ^ 1u);  // consumers released this stage's previous use
+    if (dyn) tix[s] = (uint32_t)w;  // published by the arrive below (release)
     uint8_t* buf = ring + (size_t)s * a.stage_stride;
     if (PRE) {  // the tile's codes: one bulk copy from the padded code array (16-B granules)
       const uint64_t lo = ((d.k_begin + ti) * a.tile * CB) / 8u;
@@ -233,6 +253,11 @@ __device__ void produce(const LaunchParams<CAP>& P, uint8_t* ring, uint64_t* ful
       ph ^= 1u;
       wrapped = true;
     }
+  }
+  if (dyn) {  // end of work: the next stage carries the sentinel (no bytes)
+    if (wrapped) mbar_wait_sleep(&empty[s], ph ^ 1u);
+    tix[s] = kNoItem;
+    mbar_arrive(&full[s]);
   }
 }
 
@@ -958,6 +983,7 @@ __global__ void __launch_bounds__(kThreads,
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + kMaxStages;
   uint32_t* s_wt = reinterpret_cast<uint32_t*>(smem + kWarpTotOff);  // [2][W]
+  uint32_t* tix = reinterpret_cast<uint32_t*>(smem + kTixOff);       // [stages] dispatched items
   uint8_t* ring = smem + a.ring_off;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -971,7 +997,7 @@ __global__ void __launch_bounds__(kThreads,
   __syncthreads();
 
   if (warp == kConsumerWarps) {
-    if (lane == 0) produce<EPI, CAP, is_prepacked(STRAT), code_bits(STRAT)>(P, ring, full, empty);
+    if (lane == 0) produce<EPI, CAP, is_prepacked(STRAT), code_bits(STRAT)>(P, ring, full, empty, tix);
     return;
   }
 
@@ -994,9 +1020,19 @@ __global__ void __launch_bounds__(kThreads,
   C.v[kCtrAlphaEff] = (STRAT == kFilter || STRAT == kPair) ? 0ull : 512ull * CPL;
 #endif
   WorkIter<EPI, CAP> items(P);
+  const bool dyn = EPI != kEpiWrite && a.work_ctr != nullptr;
   uint32_t k;
   uint64_t ti;
-  while (items.advance(P, k, ti)) {
+  while (true) {
+    if (dyn) {  // the stage's item, published by the producer with the stage
+      if (a.wait_ns) mbar_wait_sleep(&full[s], ph, a.wait_ns);
+      else mbar_wait(&full[s], ph);
+      const uint32_t w = tix[s];
+      if (w == kNoItem) break;
+      items.map(P, w, k, ti);
+    } else if (!items.advance(P, k, ti)) {
+      break;
+    }
     C.add(kCtrWarpTiles, 1);
     if (EPI != kEpiWrite && k != kc) {  // flush pattern kc (warp-uniform; k only grows here)
       const uint32_t ws = __reduce_add_sync(0xFFFFFFFFu, acc);
@@ -1006,8 +1042,10 @@ __global__ void __launch_bounds__(kThreads,
     }
     const PatDesc& d = P.d[k];
     const uint64_t item = d.item_base + ti;
-    if (a.wait_ns) mbar_wait_sleep(&full[s], ph, a.wait_ns);
-    else mbar_wait(&full[s], ph);
+    if (!dyn) {
+      if (a.wait_ns) mbar_wait_sleep(&full[s], ph, a.wait_ns);
+      else mbar_wait(&full[s], ph);
+    }
     const uint8_t* buf = ring + (size_t)s * a.stage_stride;
     const Pat pt{d.m, d.r, d.a1, d.bc1, d.s2, d.bc2, d.pre, (d.flags >> 8) & 0xFFu, d.stage_len, P.e + d.tbl};
     const bool edge = ti < d.edge_lo || ti >= d.edge_hi;  // tile holds invalid alignments

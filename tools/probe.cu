@@ -26,12 +26,15 @@ __global__ void ldg_kernel(const uint4* __restrict__ p, uint64_t n16, uint32_t* 
   if (acc == 0x12345678u) out[0] = acc;
 }
 
+// ctr != nullptr: tiles are fetched from that counter by the producer (dynamic dispatch)
+// and handed to the consumers through tix[stage]; ~0 ends the ring
 __global__ void tma_kernel(const uint8_t* __restrict__ base, uint64_t ntiles, uint32_t tile, uint32_t stages,
-                           uint32_t splits, uint32_t* out) {
+                           uint32_t splits, uint32_t* out, unsigned long long* ctr) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + 16;
-  uint8_t* ring = smem + 256;
+  uint64_t* tix = empty + 16;
+  uint8_t* ring = smem + 512;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x / 32 - 1;
   if (threadIdx.x == 0) {
@@ -48,13 +51,22 @@ __global__ void tma_kernel(const uint8_t* __restrict__ base, uint64_t ntiles, ui
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     uint32_t s = 0, ph = 0;
     bool wrapped = false;
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (uint64_t t0 = blockIdx.x;; t0 += gridDim.x) {
+      const uint64_t t = ctr ? atomicAdd(ctr, 1ull) : t0;
       if (wrapped) {
         uint32_t ok = 0;
         while (!ok)
           asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0,1,0,p;\n\t}"
                        : "=r"(ok) : "r"(smem_u32(&empty[s])), "r"(ph ^ 1u), "r"(20000u) : "memory");
       }
+      if (t >= ntiles) {
+        if (ctr) {
+          tix[s] = ~0ull;
+          asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(&full[s])) : "memory");
+        }
+        break;
+      }
+      tix[s] = t;
       asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
                        smem_u32(&full[s])), "r"(tile) : "memory");
       const uint32_t part = tile / splits;
@@ -68,11 +80,12 @@ __global__ void tma_kernel(const uint8_t* __restrict__ base, uint64_t ntiles, ui
     return;
   }
   uint32_t s = 0, ph = 0, acc = 0;
-  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  for (uint64_t t = blockIdx.x; ctr || t < ntiles; t += gridDim.x) {
     uint32_t ok = 0;
     while (!ok)
       asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0,1,0,p;\n\t}"
                    : "=r"(ok) : "r"(smem_u32(&full[s])), "r"(ph) : "memory");
+    if (ctr && tix[s] == ~0ull) break;
     acc ^= reinterpret_cast<const uint32_t*>(ring + (size_t)s * tile)[warp * 32 + lane];
     __syncwarp();
     if (lane == 0) asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(&empty[s])) : "memory");
@@ -105,11 +118,16 @@ extern "C" float probe_ldg(const void* p, uint64_t n, int blocks_per_sm, int rep
 }
 
 extern "C" float probe_tma(const void* p, uint64_t n, uint32_t tile, uint32_t stages, uint32_t ctas_per_sm,
-                           uint32_t splits, int consumer_warps, int reps) {
+                           uint32_t splits, int consumer_warps, int reps, int dyn) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  size_t smem = 256 + (size_t)tile * stages;
+  size_t smem = 512 + (size_t)tile * stages;
+  unsigned long long* ctr = nullptr;
+  if (dyn) {
+    cudaMalloc(&ctr, 8 * (reps + 1));
+    cudaMemset(ctr, 0, 8 * (reps + 1));
+  }
   if (cudaFuncSetAttribute(tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return -1.f;
   uint32_t* out;
@@ -119,16 +137,18 @@ extern "C" float probe_tma(const void* p, uint64_t n, uint32_t tile, uint32_t st
   cudaEventCreate(&b);
   const uint64_t ntiles = n / tile;
   const int threads = (consumer_warps + 1) * 32;
-  tma_kernel<<<sms * ctas_per_sm, threads, smem>>>((const uint8_t*)p, ntiles, tile, stages, splits, out);
+  tma_kernel<<<sms * ctas_per_sm, threads, smem>>>((const uint8_t*)p, ntiles, tile, stages, splits, out, ctr);
   cudaEventRecord(a);
   for (int r = 0; r < reps; ++r)
-    tma_kernel<<<sms * ctas_per_sm, threads, smem>>>((const uint8_t*)p, ntiles, tile, stages, splits, out);
+    tma_kernel<<<sms * ctas_per_sm, threads, smem>>>((const uint8_t*)p, ntiles, tile, stages, splits, out,
+                                                     ctr ? ctr + 1 + r : nullptr);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms = 0;
   cudaEventElapsedTime(&ms, a, b);
   cudaError_t e = cudaGetLastError();
   cudaFree(out);
+  if (ctr) cudaFree(ctr);
   if (e != cudaSuccess) return -2.f;
   return (float)(ntiles * (double)tile * reps / (ms * 1e-3) / 1e9);
 }

@@ -13,7 +13,7 @@ if __name__ == "__main__":
     lib.probe_ldg.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int]
     lib.probe_tma.restype = ctypes.c_float
     lib.probe_tma.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
-                              ctypes.c_uint32, ctypes.c_int, ctypes.c_int]
+                              ctypes.c_uint32, ctypes.c_int, ctypes.c_int, ctypes.c_int]
     res = {}
     for n in (1 << 28, 1 << 32):
         t = torch.empty(n, dtype=torch.uint8, device="cuda")
@@ -25,7 +25,7 @@ if __name__ == "__main__":
                                           (16384, 4, 3, 1), (8192, 8, 3, 1), (65536, 3, 1, 1), (32768, 6, 1, 1),
                                           (16384, 12, 1, 1)]:
             res[f"tma n={n>>20}MiB tile={tile} st={stages} ctas={ctas} split={splits}"] = round(
-                lib.probe_tma(p, n, tile, stages, ctas, splits, 8, 10), 1)
+                lib.probe_tma(p, n, tile, stages, ctas, splits, 8, 10, 0), 1)
         del t
         torch.cuda.empty_cache()
     for k, v in res.items():
