@@ -164,6 +164,8 @@ struct Tunables {
   uint32_t max_stages_pre = 6;  // their ring depth (3 CTAs x 6 stages of <= 9 KiB fit the SM)
   bool dispatch = true;         // batch calls: work items fetched from a counter (search.cuh work_ctr)
   uint64_t dispatch_min_bytes = 64ull << 20;  // ... when the call streams at least this much text (n x P)
+  uint64_t dispatch_min_bytes_single = 512ull << 20;  // single-pattern calls (the counter's memset
+                                                      // costs more than it gains on short launches)
 };
 
 const Tunables& tunables() {
@@ -186,6 +188,8 @@ const Tunables& tunables() {
     if (const char* e = std::getenv("SMGPU_CTAS_PRE")) x.ctas_pre = std::atoi(e);
     if (const char* e = std::getenv("SMGPU_DISPATCH")) x.dispatch = std::atoi(e) != 0;
     if (const char* e = std::getenv("SMGPU_DISPATCH_MIN_MB")) x.dispatch_min_bytes = (uint64_t)std::atoll(e) << 20;
+    if (const char* e = std::getenv("SMGPU_DISPATCH_MIN_MB_SINGLE"))
+      x.dispatch_min_bytes_single = (uint64_t)std::atoll(e) << 20;
     if (x.ctas_pre < 1 || x.ctas_pre > 4) x.ctas_pre = 3;
     if (const char* e = std::getenv("SMGPU_STAGES_PRE")) x.max_stages_pre = (uint32_t)std::atoi(e);
     if (x.max_stages_pre < 2 || x.max_stages_pre > (uint32_t)kMaxStages) x.max_stages_pre = 6;
@@ -195,6 +199,12 @@ const Tunables& tunables() {
     return x;
   }();
   return t;
+}
+
+// counter-dispatched work items (search.cuh work_ctr) for calls streaming enough text
+bool use_dispatch(uint64_t n, size_t P) {
+  const Tunables& tu = tunables();
+  return tu.dispatch && n * P >= (P == 1 ? tu.dispatch_min_bytes_single : tu.dispatch_min_bytes);
 }
 
 struct Plan {
@@ -602,6 +612,16 @@ sm_status enqueue_count(const uint8_t* p, size_t m, const uint8_t* t, size_t n, 
   if (s != SM_OK) return s;
   HostLaunch L;
   build_launch({&q}, t, n, UINT64_MAX, kEpiCount, L);
+  if (use_dispatch(n, 1) && L.a.total_work < kNoItem) {
+    keep_pool_cached();
+    unsigned long long* work = nullptr;
+    SM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&work), 8, st), "cudaMallocAsync(work counter)");
+    cudaError_t e = cudaMemsetAsync(work, 0, 8, st);
+    L.a.work_ctr = work;
+    sm_status r = e == cudaSuccess ? launch_checked(L, st, "search kernel") : cuda_fail(e, "cudaMemsetAsync");
+    cudaFreeAsync(work, st);
+    return r;
+  }
   return launch_checked(L, st, "search kernel");
 }
 
@@ -631,7 +651,7 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
   // (a call makes at most P + 7 launches: every flush holds >= 1 pattern)
   unsigned long long* work = nullptr;
   size_t nwork = 0, used_work = 0;
-  if (tunables().dispatch && (uint64_t)n * P >= tunables().dispatch_min_bytes) {
+  if (use_dispatch(n, P)) {
     keep_pool_cached();
     nwork = P + 8;
     SM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&work), nwork * 8, st), "cudaMallocAsync(work counters)");
@@ -802,7 +822,7 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
   unsigned long long* expand_work = stage_used + 1;
   unsigned long long* work = reinterpret_cast<unsigned long long*>(q + 16);  // [nL] pass-1 dispatch counters
   uint32_t* ovf_n = reinterpret_cast<uint32_t*>(q + 16 + nL * 8); q += ctr_b;
-  const bool dispatch = tunables().dispatch && (uint64_t)n * P >= tunables().dispatch_min_bytes;
+  const bool dispatch = use_dispatch(n, P);
   uint64_t* offsets = reinterpret_cast<uint64_t*>(q); q += offs_b;
   uint32_t* ovf_items = reinterpret_cast<uint32_t*>(q); q += ovf_b;
   void* temp = q; q += temp_b;

@@ -39,6 +39,11 @@ for alpha in (b"ACGT", b"\x00\x01", bytes(range(32, 127)), b"a"):
                 wp = np.concatenate([oracle.naive_report(p, a) for p in pats]) if pats else np.zeros(0)
                 fails += not np.array_equal(pos[:cap].cpu().numpy().astype(np.uint64), wp.astype(np.uint64))
             fails += sm.sm_histogram(t).cpu().numpy().astype(np.uint64).tolist() != h.tolist()
+            for p in pats[:2]:  # the single-pattern entry points (their own launch path)
+                fails += sm.sm_count(p, t) != oracle.naive_count(p, a)
+                got, tot = sm.sm_report(p, t)
+                fails += tot != oracle.naive_count(p, a) or not np.array_equal(
+                    got.cpu().numpy().astype(np.uint64), oracle.naive_report(p, a).astype(np.uint64))
 torch.cuda.synchronize()
 print("sanitize workload done, mismatches:", fails)
 sys.exit(1 if fails else 0)
