@@ -183,8 +183,9 @@ sm_status sm_report_async(const uint8_t* p, size_t m, const uint8_t* t, size_t n
 /* Enqueue the reporting version for P patterns (see sm_count_batch for p, m,
  * max_alignments, hist, strategy, and the code-array scratch).  One read of the text
  * per pattern: matches are staged compactly (scratch from the stream-ordered pool:
- * ~24 B per (pattern, 32 KiB tile) plus a staging pool of min(2 GiB, 64 MiB + 4 cap)
- * bytes, SMGPU_STAGE_BYTES overrides), then expanded; tiles that do not fit the pool
+ * ~24 B per (pattern, 32 KiB tile) plus a staging pool of min(4 GiB, 64 MiB +
+ * min(16 cap, 4.2 KiB per (pattern, tile)) + 38 KiB per SM per launch) bytes, mostly
+ * untouched; SMGPU_STAGE_BYTES overrides), then expanded; tiles that do not fit the pool
  * are recomputed from the text -- never a different result.  d_counts[i] (DEVICE u64[P]) = count of p[i];
  * positions of all patterns are written CONCATENATED in pattern order into DEVICE
  * pos[0..cap): pattern i's ascending positions start at sum_{j<i} d_counts[j].

@@ -704,16 +704,23 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
   return SM_OK;
 }
 
-// Staging pool of the reporting pass (bytes): enough for ~4 bytes per reported
-// position plus 64 MiB, at most 2 GiB; SMGPU_STAGE_BYTES overrides (tests force the
-// overflow path with a tiny pool).  Tiles whose record does not fit are recomputed
-// from the text by the overflow pass, so the size never changes results.
-uint64_t stage_pool_bytes(uint64_t cap) {
+// Staging pool of the reporting pass (bytes).  Records: at most 16 B per reported
+// position (a sparse record = 16-B header + 16-B list per match) and at most one
+// 528-B bitmap record per warp-tile; plus, per launch, one partly used 8 KiB chunk
+// per resident compare warp (a warp's chunk is not handed on to the next launch);
+// 64 MiB slack; at most 4 GiB.  SMGPU_STAGE_BYTES overrides (tests force the overflow
+// path with a tiny pool).  Tiles whose record does not fit are recomputed from the
+// text by the overflow pass, so the size never changes results (the memory is
+// allocated per call from the stream-ordered pool, not written beyond what is used).
+uint64_t stage_pool_bytes(uint64_t cap, uint64_t items, uint64_t launches) {
   static const long long env = [] {
     const char* e = std::getenv("SMGPU_STAGE_BYTES");
     return e ? std::atoll(e) : -1LL;
   }();
-  uint64_t b = env >= 0 ? (uint64_t)env : std::min<uint64_t>(2ull << 30, (64ull << 20) + 4 * cap);
+  const uint64_t warps = (uint64_t)num_sms() * 4u * kConsumerWarps;  // >= resident compare warps
+  const uint64_t records = std::min<uint64_t>(16ull * cap, items * kConsumerWarps * 528ull);
+  const uint64_t partial = launches * warps * (uint64_t)kStageChunk * 16u;
+  uint64_t b = env >= 0 ? (uint64_t)env : std::min<uint64_t>(4ull << 30, (64ull << 20) + records + partial);
   return (b + 15) & ~15ull;
 }
 
@@ -810,7 +817,7 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
   const uint64_t nL = Ls.size();
   const uint64_t wc_b = al(items * 16), offs_b = al(items * 8), bits_b = al((items + 31) / 32 * 4),
                  ovf_b = al(items * 4), ctr_b = al(16 + nL * 12), temp_b = al(temp_bytes),
-                 stage_b = stage_pool_bytes(cap);
+                 stage_b = stage_pool_bytes(cap, items, nL);
   uint8_t* scratch = nullptr;
   SM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&scratch),
                               wc_b + bits_b + ctr_b + offs_b + ovf_b + temp_b + stage_b, st),
