@@ -8,9 +8,10 @@
 //
 // One warp per pool chunk (8 KiB): the chunk is pulled into shared memory with
 // independent 16-B loads, lane 0 walks its record chain (up to the zero terminator),
-// the lanes fetch the records' output offsets in parallel, then each record is
-// written: u16 lists lane-parallel, bitmaps 32 x 32 alignments per round through a
-// shared index buffer, so that the 8-byte position stores are coalesced.
+// the lanes fetch the records' output offsets in parallel, then the u16 lists of all
+// the chunk's records are written as one flattened sequence (32 consecutive elements
+// per warp store), and bitmap records 32 x 32 alignments per round through a shared
+// index buffer, so that the 8-byte position stores are coalesced.
 #include "device_util.cuh"
 #include "launch.h"
 
@@ -20,7 +21,8 @@ namespace {
 constexpr int kExpandWarps = 8;
 constexpr uint32_t kChunkBytes = kStageChunk * 16u;
 constexpr uint32_t kMaxRecs = kStageChunk / 2u;  // a record is >= 2 units (header + data)
-constexpr uint32_t kWarpSmem = kChunkBytes + kMaxRecs * (8u + 2u) + 2048u;
+// per warp: chunk | rout u64[kMaxRecs] | rpre u32[kMaxRecs + 1] | roff u16[kMaxRecs] | sbuf u16[1024]
+constexpr uint32_t kWarpSmem = (kChunkBytes + kMaxRecs * 8u + (kMaxRecs + 1u) * 4u + kMaxRecs * 2u + 2048u + 15u) & ~15u;
 
 __device__ __forceinline__ uint32_t warp_incl_scan_x(uint32_t v, int lane) {
 #pragma unroll
@@ -31,20 +33,18 @@ __device__ __forceinline__ uint32_t warp_incl_scan_x(uint32_t v, int lane) {
   return v;
 }
 
-__device__ __forceinline__ void write_record(const uint8_t* rec, uint64_t out, uint64_t* pos, uint64_t cap,
+__device__ __forceinline__ bool is_list_record(uint32_t hw) {
+  return 2u * (hw & 0xFFFFu) < (512u << (hw >> 24)) / 8u;  // 2 count < wspan / 8
+}
+
+// a bitmap record: bit b of u32 word i <-> u = w wspan + 32 i + b
+__device__ __forceinline__ void write_bitmap(const uint8_t* rec, uint64_t out, uint64_t* pos, uint64_t cap,
                                              uint16_t* sbuf, int lane) {
   const uint4 h = *reinterpret_cast<const uint4*>(rec);
   const int64_t pos_base = (int64_t)(((uint64_t)h.y << 32) | h.x);
-  const uint32_t c = h.w & 0xFFFFu, w = (h.w >> 16) & 0xFFu;
+  const uint32_t w = (h.w >> 16) & 0xFFu;
   const uint32_t wspan = 512u << (h.w >> 24);
   const uint8_t* data = rec + kRecHeader;
-  if (2u * c < wspan / 8u) {  // u16 list
-    const uint16_t* L = reinterpret_cast<const uint16_t*>(data);
-    for (uint32_t i = lane; i < c; i += 32)
-      if (out + i < cap) pos[out + i] = (uint64_t)(pos_base + (int64_t)L[i]);
-    return;
-  }
-  // bitmap: bit b of u32 word i <-> u = w wspan + 32 i + b
   const uint32_t* bm = reinterpret_cast<const uint32_t*>(data);
   const uint32_t words = wspan / 32u;
   uint64_t o = out;
@@ -92,7 +92,7 @@ __device__ __forceinline__ void write_record(const uint8_t* rec, uint64_t out, u
   }
 }
 
-__global__ void __launch_bounds__(kExpandWarps * 32) stage_expand_kernel(const uint8_t* stage,
+__global__ void __launch_bounds__(kExpandWarps * 32, 2) stage_expand_kernel(const uint8_t* stage,
                                                                         const unsigned long long* stage_used,
                                                                         uint64_t cap16, const uint16_t* wc,
                                                                         const uint64_t* tile_offsets, uint64_t* pos,
@@ -101,7 +101,8 @@ __global__ void __launch_bounds__(kExpandWarps * 32) stage_expand_kernel(const u
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* cbuf = xsm + warp * kWarpSmem;                                    // the chunk
   uint64_t* rout = reinterpret_cast<uint64_t*>(cbuf + kChunkBytes);           // [kMaxRecs] output offsets
-  uint16_t* roff = reinterpret_cast<uint16_t*>(rout + kMaxRecs);              // [kMaxRecs] record offsets (units)
+  uint32_t* rpre = reinterpret_cast<uint32_t*>(rout + kMaxRecs);              // [kMaxRecs + 1] list-element prefix
+  uint16_t* roff = reinterpret_cast<uint16_t*>(rpre + kMaxRecs + 1);          // [kMaxRecs] record offsets (units)
   uint16_t* sbuf = roff + kMaxRecs;                                           // [1024] bitmap expansion
   const unsigned long long used = *stage_used < cap16 ? *stage_used : cap16;
   const uint64_t nchunks = (used + kStageChunk - 1) / kStageChunk;
@@ -147,6 +148,7 @@ __global__ void __launch_bounds__(kExpandWarps * 32) stage_expand_kernel(const u
         if (r < nrec) {
           const uint4 h = *reinterpret_cast<const uint4*>(cbuf + roff[r] * 16u);
           wv[u] = (h.w >> 16) & 0xFFu;
+          rpre[r] = is_list_record(h.w) ? (h.w & 0xFFFFu) : 0u;
           v[u] = reinterpret_cast<const uint4*>(wc)[h.z];
           off[u] = tile_offsets[h.z];
         }
@@ -165,9 +167,46 @@ __global__ void __launch_bounds__(kExpandWarps * 32) stage_expand_kernel(const u
       }
     }
     __syncwarp();
-    for (uint32_t r = 0; r < nrec; ++r) {
+    // u16-list records, flattened: element e of the chunk's concatenated lists goes to
+    // lane e mod 32, so a warp store covers 32 consecutive elements (1-3 records of a
+    // sparse chunk) instead of one record's few positions
+    uint32_t carry = 0;
+    for (uint32_t b = 0; b < nrec; b += 32) {  // exclusive prefix of the list lengths
+      const uint32_t v = b + lane < nrec ? rpre[b + lane] : 0u;
+      const uint32_t incl = warp_incl_scan_x(v, lane);
+      if (b + lane < nrec) rpre[b + lane] = carry + incl - v;
+      carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
+    }
+    if (lane == 0) rpre[nrec] = carry;
+    __syncwarp();
+    {
+      uint32_t r = 0, r_beg = 0, r_end = nrec ? rpre[1] : 0u;
+      bool fresh = true;
+      uint64_t out0 = 0;
+      int64_t base = 0;
+      const uint16_t* L = nullptr;
+      for (uint32_t e = lane; e < carry; e += 32) {
+        while (e >= r_end) {  // lanes only move forward through the records
+          ++r;
+          r_end = rpre[r + 1];
+          fresh = true;
+        }
+        if (fresh) {
+          const uint8_t* rec = cbuf + roff[r] * 16u;
+          const uint2 hb = *reinterpret_cast<const uint2*>(rec);
+          base = (int64_t)(((uint64_t)hb.y << 32) | hb.x);
+          L = reinterpret_cast<const uint16_t*>(rec + kRecHeader);
+          out0 = rout[r];
+          r_beg = rpre[r];
+          fresh = false;
+        }
+        const uint32_t i = e - r_beg;
+        if (out0 + i < cap) pos[out0 + i] = (uint64_t)(base + (int64_t)L[i]);
+      }
+    }
+    for (uint32_t r = 0; r < nrec; ++r) {  // bitmap records (no list elements)
       const uint64_t out = rout[r];
-      if (out < cap) write_record(cbuf + roff[r] * 16u, out, pos, cap, sbuf, lane);
+      if (rpre[r + 1] == rpre[r] && out < cap) write_bitmap(cbuf + roff[r] * 16u, out, pos, cap, sbuf, lane);
     }
     __syncwarp();  // cbuf / rout are reused for the next chunk
   }
