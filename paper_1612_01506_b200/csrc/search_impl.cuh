@@ -933,14 +933,26 @@ __device__ __forceinline__ void stage_warp(const LaunchArgs& a, const PatDesc& d
       const uint32_t incl = warp_incl_scan(pc, lane);
       uint32_t idx = incl - pc;
       const uint32_t u0 = (uint32_t)warp * kWspan + 16u * (uint32_t)lane * CPL;
+      // the lane's CPL 16-bit masks as one bit string (bit 16 j + k <-> alignment u0 + 16 j + k),
+      // extracted in one loop: the warp iterates max-over-lanes(popcount) times, not once
+      // per (chunk with a match in any lane)
+      static_assert(CPL <= 8, "list extraction holds at most 128 mask bits per lane");
+      uint64_t lo = 0, hi = 0;
 #pragma unroll
       for (int j = 0; j < CPL; ++j) {
-        uint32_t m = mk[j];
-        while (m) {
-          const uint32_t b = __ffs(m) - 1;
-          m &= m - 1;
-          bm[idx++] = (uint16_t)(u0 + 16u * j + b);
+        if (j < 4) lo |= (uint64_t)mk[j] << (16 * j);
+        else hi |= (uint64_t)mk[j] << (16 * (j - 4));
+      }
+      while (lo | hi) {
+        uint32_t b;
+        if (lo) {
+          b = (uint32_t)__ffsll((long long)lo) - 1u;
+          lo &= lo - 1;
+        } else {
+          b = 64u + (uint32_t)__ffsll((long long)hi) - 1u;
+          hi &= hi - 1;
         }
+        bm[idx++] = (uint16_t)(u0 + b);
       }
       __syncwarp();
       const uint4* src = reinterpret_cast<const uint4*>(bm);  // coalesced 16-B copy of the list
