@@ -217,11 +217,15 @@ struct Plan {
 };
 
 
-void choose_tiling(uint64_t n, Plan& pl) {
+// P = patterns of the call: a launch holds up to kMaxBatch of them, each a full pass,
+// so its work items are tiles x min(P, kMaxBatch)
+void choose_tiling(uint64_t n, size_t P, Plan& pl) {
   const uint64_t sms = (uint64_t)num_sms();
+  const uint64_t per_launch = std::max<uint64_t>(1, std::min<uint64_t>(P, kMaxBatch));
   pl.tile = tunables().tile;
   // small texts: shrink the tile until every CTA slot gets work
-  while (pl.tile > 4096 && (n + pl.tile - 1) / pl.tile < sms * (uint64_t)tunables().ctas_per_sm) pl.tile /= 2;
+  while (pl.tile > 4096 && (n + pl.tile - 1) / pl.tile * per_launch < sms * (uint64_t)tunables().ctas_per_sm)
+    pl.tile /= 2;
   pl.cpl = (int)(pl.tile / (16u * kLanesPerTilePass));
 }
 
@@ -321,14 +325,14 @@ struct TextInfo {
   double total = 0;         // n from the histogram
   int code_b = 0;           // text_code_bits: 0, 1 or 2
   uint32_t code_shift = 0;
-  Plan tiling;              // choose_tiling(n): tile and CPL
+  Plan tiling;              // choose_tiling(n, P): tile and CPL
 };
 
-TextInfo text_info(const uint64_t* hist, uint64_t n) {
+TextInfo text_info(const uint64_t* hist, uint64_t n, size_t P = 1) {
   TextInfo t;
   for (int c = 0; c < 256; ++c) t.total += (double)hist[c];
   t.code_b = text_code_bits(hist, &t.code_shift);
-  choose_tiling(n, t.tiling);
+  choose_tiling(n, P, t.tiling);
   return t;
 }
 
@@ -646,7 +650,7 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
   if (pe != cudaSuccess) return cuda_fail(pe, "prepack");
   // plan and launch as we go: a batch is launched as soon as it is full, so the GPU
   // starts on the first patterns while the host still orders the later ones
-  const TextInfo tinfo = text_info(h, n);
+  const TextInfo tinfo = text_info(h, n, P);
   // counter-dispatched work items for long calls: one zeroed counter per launch
   // (a call makes at most P + 7 launches: every flush holds >= 1 pattern)
   unsigned long long* work = nullptr;
@@ -752,7 +756,7 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
   cudaError_t pe = cudaSuccess;
   CodeArray codes{prepack_text(h, t, n, P, st, &cb, &pe), st};
   if (pe != cudaSuccess) return cuda_fail(pe, "prepack");
-  const TextInfo tinfo = text_info(h, n);
+  const TextInfo tinfo = text_info(h, n, P);
   std::vector<Planned> plans;
   plans.reserve(P);
   for (size_t i = 0; i < P; ++i) {
