@@ -145,6 +145,12 @@ def _text(t) -> Tuple[int, int]:
 def _stream(stream) -> int:
     import torch
     if stream is None:
+        # torch's current stream of the current device; the raw-handle query avoids the
+        # ~15 us of Python device bookkeeping in torch.cuda.current_stream() (host-bound
+        # small calls, tools/host_overhead.py)
+        raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+        if raw is not None:
+            return raw(torch._C._cuda_getDevice())
         return torch.cuda.current_stream().cuda_stream
     if isinstance(stream, int):
         return stream

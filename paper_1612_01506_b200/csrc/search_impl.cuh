@@ -897,7 +897,7 @@ struct StageAlloc {
 // terminator header.  No other warp is waited for.  If the pool is exhausted the item
 // is queued (once) for the overflow pass, which recomputes it from the text.
 template <int CPL, bool CLEAN>
-__device__ __forceinline__ void stage_warp(const LaunchArgs& a, const PatDesc& d, uint16_t* bm, StageAlloc& al,
+__device__ __forceinline__ void stage_warp(const LaunchArgs& a, uint16_t* bm, StageAlloc& al,
                                            int warp, int lane, uint64_t item, int64_t pos_base, uint32_t wcnt) {
   constexpr uint32_t kWspan = 512u * CPL;  // alignments per warp (32 lanes x CPL chunks x 16)
   constexpr uint32_t kLog2Cpl = CPL == 8 ? 3 : CPL == 4 ? 2 : CPL == 2 ? 1 : 0;
@@ -1089,7 +1089,7 @@ __global__ void __launch_bounds__(kThreads,
         released = true;
         acc += sk.n;
         const uint32_t wcnt = __reduce_add_sync(0xFFFFFFFFu, sk.n);
-        if (wcnt) stage_warp<CPL, true>(a, d, list, salloc, warp, lane, item, pos_base, wcnt);
+        if (wcnt) stage_warp<CPL, true>(a, list, salloc, warp, lane, item, pos_base, wcnt);
       } else {  // overflow pass: buffer this warp's matches, exchange warp totals, write coalesced
         AppendSink<true> as{list};
         ftile(as, C);
@@ -1134,7 +1134,7 @@ __global__ void __launch_bounds__(kThreads,
             else list[rel] = (uint16_t)mk[it];
           }
           __syncwarp();
-          stage_warp<CPL, false>(a, d, list, salloc, warp, lane, item, pos_base, wcnt);
+          stage_warp<CPL, false>(a, list, salloc, warp, lane, item, pos_base, wcnt);
         }
       } else {
         write_units<CPL>(a, s_wt, list, par, warp, lane, item, pos_base, mk, mbase, units);
@@ -1158,7 +1158,7 @@ __global__ void __launch_bounds__(kThreads,
 #pragma unroll
           for (int it = 0; it < CPL; ++it) list[it * 32 + lane] = (uint16_t)g_to_mask16(g[it]);
           __syncwarp();
-          stage_warp<CPL, false>(a, d, list, salloc, warp, lane, item, pos_base, wcnt);
+          stage_warp<CPL, false>(a, list, salloc, warp, lane, item, pos_base, wcnt);
         }
       } else {
         write_masks<true, CPL>(a, s_wt, list, par, warp, lane, item, cw0, pos_base, g);
