@@ -26,8 +26,19 @@ if __name__ == "__main__":
                                           (16384, 12, 1, 1)]:
             res[f"tma n={n>>20}MiB tile={tile} st={stages} ctas={ctas} split={splits}"] = round(
                 lib.probe_tma(p, n, tile, stages, ctas, splits, 8, 10, 0), 1)
+            if splits == 1:  # tiles fetched from a counter (the search kernel's dispatch for long calls)
+                res[f"tma-dyn n={n>>20}MiB tile={tile} st={stages} ctas={ctas}"] = round(
+                    lib.probe_tma(p, n, tile, stages, ctas, 1, 8, 10, 1), 1)
         del t
         torch.cuda.empty_cache()
     for k, v in res.items():
         print(f"{k:60s} {v:8.1f} GB/s")
-    print(json.dumps(res))
+    key = "tma-dyn n=4096MiB tile=32768 st=2 ctas=3"
+    out = {"source": "tools/probe.py on one B200 (gpurun), read-only streaming without compute, best of 10, CUDA events",
+           "read_stream_GBps": res[key],
+           "config_of_read_stream": "TMA 1-D bulk ring, 32 KiB tiles x 2 stages x 3 CTAs/SM, tiles fetched from a "
+                                    "counter (the search kernel's configuration and dispatch), 4 GiB",
+           "all": res}
+    if len(sys.argv) > 1:
+        json.dump(out, open(sys.argv[1], "w"), indent=1)
+    print(json.dumps(out))
