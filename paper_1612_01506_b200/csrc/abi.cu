@@ -366,12 +366,14 @@ sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist
     // Chunk-test hit rates (i.i.d. estimate from the histogram): FILTER queues the 16-byte
     // chunks holding p[pi(1)] (h1), PAIR those with a pi(1)&pi(2) survivor (h12); each
     // queued chunk costs a gather + two exact compares.  BLOCK (Alg. 4 over warp-blocks)
-    // has a flat cost and wins only when even the pair test passes most chunks.
+    // has a flat cost and wins only when even the pair test passes most chunks (m >= 3).
     // Crossovers measured on B200 (tools/pair_sweep.sh, profiles/strategy_r1.md).
     const double f1 = freq(0), f12 = m >= 2 ? f1 * freq(1) : f1;
     const double h1 = 1.0 - std::pow(1.0 - f1, 16.0), h12 = 1.0 - std::pow(1.0 - f12, 16.0);
     if (h12 > tunables().block_min_hit) {
-      strategy = kBlock;
+      // m = 2: PAIR's pair test, taken per byte, is the match itself (one pass, no queue,
+      // no phase B: search_impl.cuh filter_tile_q), so it replaces BLOCK at any density
+      strategy = m == 2 ? kPair : kBlock;
       if (tunables().auto_packed) {  // small text alphabet: compare b-bit codes
         const int pk = packed();
         if (pk) strategy = pk;

@@ -272,11 +272,11 @@ __device__ __forceinline__ bool chunk_hit(const uint4 v, uint32_t bc) {
 // (t[x + pi(1)] ^ p[pi(1)]) | (t[x + pi(2)] ^ p[pi(2)]) is zero iff alignment x matches
 // both, so one borrow-based zero-byte test on the OR covers the two comparisons
 // (exact as a whole-chunk predicate, like chunk_hit).  QA = word offset of pi(2)'s window.
-template <int QA, bool WORD_ALIGNED = false>
-__device__ __forceinline__ bool pair_hit(const uint8_t* buf, uint32_t c, uint32_t pre, uint32_t s2, uint32_t bc1,
-                                         uint32_t bc2) {
-  const uint4 v1 = lds128(buf + pre + 16u * c);
-  uint4 v2;
+// the pi(1) bytes and pi(2) bytes of chunk c's 16 alignments (see pair_hit)
+template <int QA, bool WORD_ALIGNED>
+__device__ __forceinline__ void pair_windows(const uint8_t* buf, uint32_t c, uint32_t pre, uint32_t s2, uint4& v1,
+                                             uint4& v2) {
+  v1 = lds128(buf + pre + 16u * c);
   if constexpr (WORD_ALIGNED) {  // pi(2)'s window starts on a word: no funnel shifts
     if constexpr (QA == 0) {
       v2 = lds128(buf + 16u * c + (s2 & ~15u));
@@ -289,6 +289,13 @@ __device__ __forceinline__ bool pair_hit(const uint8_t* buf, uint32_t c, uint32_
   } else {
     v2 = window16_q<QA>(buf + 16u * c + (s2 & ~15u), (s2 & 3u) * 8u);
   }
+}
+
+template <int QA, bool WORD_ALIGNED = false>
+__device__ __forceinline__ bool pair_hit(const uint8_t* buf, uint32_t c, uint32_t pre, uint32_t s2, uint32_t bc1,
+                                         uint32_t bc2) {
+  uint4 v1, v2;
+  pair_windows<QA, WORD_ALIGNED>(buf, c, pre, s2, v1, v2);
   const uint32_t y0 = (v1.x ^ bc1) | (v2.x ^ bc2), y1 = (v1.y ^ bc1) | (v2.y ^ bc2);
   const uint32_t y2 = (v1.z ^ bc1) | (v2.z ^ bc2), y3 = (v1.w ^ bc1) | (v2.w ^ bc2);
   return ((((y0 - 0x01010101u) & ~y0) | ((y1 - 0x01010101u) & ~y1) | ((y2 - 0x01010101u) & ~y2) |
@@ -472,6 +479,27 @@ template <int CPL, bool PA, int QA, class Sink, bool WA = false>
 __device__ __forceinline__ void filter_tile_q(const Pat& pt, const uint8_t* buf, uint32_t cw0, int lane, uint16_t* qc,
                                               bool edge, int32_t rlo, int32_t rhi, Sink& sink, Ctr& C) {
   C.add(kCtrChunks, 32u * CPL);
+  if constexpr (PA) {
+    if (pt.m == 2) {  // warp-uniform: pi(1), pi(2) are the whole pattern, so the pair test of
+                      // phase A, taken per byte, IS the match -- one pass, no queue, no phase B
+#pragma unroll
+      for (int it = 0; it < CPL; ++it) {
+        const uint32_t c = cw0 + it * 32u + lane;
+        SMGPU_DCHECK(pt.pre + 16u * c + 16u <= pt.lim && 16u * c + (pt.s2 & ~15u) + 32u <= pt.lim);
+        uint4 v1, v2;
+        pair_windows<QA, WA>(buf, c, pt.pre, pt.s2, v1, v2);
+        Found4 F = edge ? found_from_mask16(range_mask16_rel((int32_t)(16u * c), rlo, rhi)) : found_all();
+        F.f0 &= eq_flags_raw((v1.x ^ pt.bc1) | (v2.x ^ pt.bc2), 0u);
+        F.f1 &= eq_flags_raw((v1.y ^ pt.bc1) | (v2.y ^ pt.bc2), 0u);
+        F.f2 &= eq_flags_raw((v1.z ^ pt.bc1) | (v2.z ^ pt.bc2), 0u);
+        F.f3 &= eq_flags_raw((v1.w ^ pt.bc1) | (v2.w ^ pt.bc2), 0u);
+        const uint32_t g = compress_found(F);
+        C.add(kCtrSurvivors, __popc(g));
+        sink(c, g, lane);
+      }
+      return;
+    }
+  }
   constexpr int G = CPL < kGroup ? CPL : kGroup;
 #pragma unroll
   for (int g0 = 0; g0 < CPL; g0 += G) {

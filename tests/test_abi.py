@@ -65,8 +65,9 @@ def test_plan_policy(sm):
 
 def test_plan_auto_rule(sm):
     """AUTO (abi.cu make_plan, profiles/strategy_pair_r1.md): h1 = 1-(1-f1)^16 is FILTER's chunk
-    queue rate, h12 = 1-(1-f1 f2)^16 PAIR's (h1 for m = 1); BLOCK/PACKED if h12 > 0.5, else PAIR
-    if m >= 2 and h1 > 0.2 (0.12 for m >= 32), else FILTER."""
+    queue rate, h12 = 1-(1-f1 f2)^16 PAIR's (h1 for m = 1); BLOCK/PACKED if h12 > 0.5 (PAIR
+    instead of BLOCK for m = 2, where the pair test is the match), else PAIR if m >= 2 and
+    h1 > 0.2 (0.12 for m >= 32), else FILTER."""
     h = np.zeros(256, dtype=np.uint64)
     # 20 symbols 'A'..'T': two frequent (10 % each), the rest rare
     for i, c in enumerate(range(65, 85)):
@@ -84,6 +85,8 @@ def test_plan_auto_rule(sm):
         hb[c] = 9000 if c < 67 else 500
     s, _ = sm.sm_plan(b"ABAB", hb)                 # h12 = 1-(1-0.2025)^16 ~ 0.97 > 0.5
     assert s == sm.SM_STRATEGY_BLOCK               # 6 symbols: no 2-bit code -> BLOCK
+    s, _ = sm.sm_plan(b"AB", hb)                   # m = 2: the exact one-pass PAIR replaces BLOCK
+    assert s == 5
     s, _ = sm.sm_plan(b"ABCDE", hb)                # pi(1), pi(2) = C, D (5 % each): h1 ~ 0.56 -> PAIR
     assert s == 5
     s, _ = sm.sm_plan(b"ABCDE", hb, strategy=sm.SM_STRATEGY_PAIR)
