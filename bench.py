@@ -12,6 +12,20 @@ patterns at each m in {2,4,...,1024}).  value = text bytes x patterns / step tim
 `report` sub-object.  Multi-GPU: weak scaling, each rank holds a 256 MiB shard
 of an N x 256 MiB text (+1023-byte halo) and counts its owned alignments.
 
+`--config c5` is the multi-GPU scale config of BASELINE.json (configs[4]): a 64 GiB
+text of uniform bytes, STRONG scaling -- the same 2^36-byte text is sharded over the
+N ranks (each holds its 2^36 / N owned bytes + a 63-byte halo), 200 patterns (28 of
+them per length straddle the k/8 shard cuts).
+
+`--gpus N` without a launcher re-executes itself under torch.distributed.run with N
+processes (one per GPU; refused when fewer than N GPUs are visible).  `--fused` sums
+the counts through an NVLink multicast buffer (NEXT-4) instead of an NCCL all_reduce
+where the platform provides one.
+
+Counts of a full-size config are compared, pattern by pattern, with the oracle's
+golden answers (tests/golden/<config>.json, from tools/make_golden.py); a mismatch
+fails the run.
+
 `--impl reference` times the CPU oracle (oracle/, plain Alg. 1) on the host
 cores on a bounded sample of the same workload.
 """
@@ -50,7 +64,60 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--strategy", type=int, default=0)
     ap.add_argument("--peel", type=int, default=0)
+    ap.add_argument("--fused", action="store_true", help="NVLS multicast count reduction (NEXT-4) for N > 1")
     return ap.parse_args()
+
+
+STRONG = {"c5"}  # configs whose total text is fixed as N grows (BASELINE.json configs[4])
+
+
+def maybe_relaunch(args):
+    """`bench.py --gpus N` started as a plain process: run N ranks under torch.distributed.run
+    (the driver's own launch sets WORLD_SIZE and lands in run_native directly)."""
+    if "WORLD_SIZE" in os.environ or args.gpus <= 1 or args.impl == "reference":
+        return
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but {have} CUDA device(s) visible; refusing to run "
+                         f"fewer ranks than asked\n")
+        sys.exit(2)
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
+def nccl_init_lines(path):
+    """The communicator-init lines of this rank's NCCL_DEBUG=INFO log (they name nranks)."""
+    try:
+        lines = [ln.strip() for ln in open(path, errors="replace") if "nranks" in ln and "Init COMPLETE" in ln]
+        return lines[:2]
+    except OSError:
+        return []
+
+
+def golden_check(config: str, counts, n: int, P: int):
+    """Compare every count with tests/golden/<config>.json (oracle answers, tools/make_golden.py);
+    None when the run is not the golden workload (sizes or pattern set overridden)."""
+    path = os.path.join(ROOT, "tests", "golden", f"{config}.json")
+    if not os.path.exists(path):
+        return {"golden": None, "note": f"{os.path.relpath(path, ROOT)} not written"}
+    g = json.load(open(path))
+    if g["n"] != n or len(g["cases"]) != P:
+        return None
+    want = [c["count"] for c in g["cases"]]
+    bad = [i for i, (a, b) in enumerate(zip(counts, want)) if int(a) != int(b)]
+    if bad:
+        raise SystemExit(f"bench.py: {len(bad)} of {P} counts differ from the oracle's golden answers "
+                         f"({os.path.relpath(path, ROOT)}), first pattern {bad[0]}: {int(counts[bad[0]])} != "
+                         f"{want[bad[0]]}")
+    return {"golden": os.path.relpath(path, ROOT), "patterns": P, "mismatches": 0,
+            "count_sum": int(sum(want))}
 
 
 def traffic_per_pass(config: str):
@@ -65,6 +132,13 @@ def read_probe():
     """Measured read-only streaming ceiling of the search kernel's TMA configuration (profiles/probe_r1.json)."""
     try:
         return float(json.load(open(os.path.join(ROOT, "profiles", "probe_r1.json")))["read_stream_GBps"])
+    except Exception:
+        return None
+
+
+def load_profile(name):
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", name)))
     except Exception:
         return None
 
@@ -141,8 +215,10 @@ def build_workload(args, rank: int, world: int):
     import synth
     cfg = args.config.lower()
     base = synth.text_spec(cfg)
-    n_shard = args.shard_bytes or base.n
-    N = n_shard * world
+    if cfg in STRONG:   # the total text is fixed; ranks split it
+        N = args.shard_bytes * world if args.shard_bytes else base.n
+    else:               # weak scaling: every rank holds a config-sized shard
+        N = (args.shard_bytes or base.n) * world
     spec = synth.text_spec(cfg, n=N)
     lengths = [int(x) for x in args.lengths.split(",")] if args.lengths else None
     pats = synth.patterns(cfg, spec=spec, per_m=args.per_m, lengths=lengths)
@@ -290,16 +366,33 @@ def run_native(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started {world} rank(s)")
+    if torch.cuda.device_count() <= local:
+        raise SystemExit(f"bench.py: rank {rank} needs CUDA device {local}; {torch.cuda.device_count()} visible")
     torch.cuda.set_device(local)
+    nccl_log = None
     if world > 1:
+        # NCCL's own communicator-init lines (nranks, NVLS/NVLink use) go to a per-rank log;
+        # rank 0 quotes them in its JSON line
+        nccl_log = f"/tmp/smgpu_bench_nccl.{os.getpid()}.log"
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", nccl_log)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.barrier()
     dev = torch.device("cuda", local)
     sm.load_library()
     synth.build()
 
+    cfg = args.config.lower()
+    strong = cfg in STRONG
     spec, pats = build_workload(args, rank, world)
     max_m = max(p.m for p in pats)
     shard = smd.make_shard(spec.n, rank, world, halo=max(0, max_m - 1))
+    if strong:
+        args.no_e2e = True      # a 64 GiB text: no pinned host copy of it (device-resident config)
+        args.no_report = True
     text = synth.gen_text_device(spec, shard.own_lo, shard.held_len)
     owned = text[: shard.owned_bytes]
     P = len(pats)
@@ -310,18 +403,31 @@ def run_native(args):
     stream = torch.cuda.current_stream()
 
     pbatch = sm.PatternBatch(pdata)
+    mc = None
+    if args.fused and world > 1:
+        mc = smd.MulticastCounts(P, dev)
+    fused = bool(mc is not None and mc.available)
 
     def step(ev=None):
         h = smd.global_histogram(text, shard)             # A1 (+ all_reduce)
         hh = h.cpu().numpy().astype(np.uint64)           # 2 KiB D2H for the host-side order (A2)
         if ev is not None:
             ev[0].record(stream)
+        if fused:  # NEXT-4: search + multimem.red into every rank's copy (no NCCL call)
+            c = smd.count_sharded_fused(pbatch, held, shard, hh, mc, strategy=args.strategy)
+            if ev is not None:
+                ev[1].record(stream)
+                ev[2].record(stream)
+            counts.copy_(c)
+            return hh
         # A2 (host, per pattern) + A3..A7: each pattern a full pass over the shard
         sm.sm_count_batch(pbatch, held, counts, hist=hh, max_alignments=shard.owned_bytes,
                           strategy=args.strategy)
         if ev is not None:
             ev[1].record(stream)
         smd.allreduce_sum_(counts)
+        if ev is not None:
+            ev[2].record(stream)
         return hh
 
     def barrier():
@@ -338,7 +444,7 @@ def run_native(args):
     clk.start()
     time.sleep(0.3)  # let nvidia-smi deliver its first sample before the timed region
     launches0 = sm.sm_launch_count()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    evs = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     h0 = clk.mark()
@@ -350,7 +456,8 @@ def run_native(args):
     h1 = clk.mark()
     launches = sm.sm_launch_count() - launches0
     total_ms = start.elapsed_time(end)
-    search_ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps   # the P search launches of a step
+    search_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps   # the P search launches of a step
+    coll_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps     # the count all_reduce (N > 1)
     clocks = clk.stop(h0, h1)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -385,6 +492,8 @@ def run_native(args):
     step()  # restore counts of the full step
     torch.cuda.synchronize()
     counts_host = counts.cpu().numpy()
+    # every global count vs the oracle's golden answer (1 GPU, or the strong-scaling c5 at any N)
+    parity = golden_check(cfg, counts_host, spec.n, P) if (world == 1 or strong) else None
 
     # ---------------- end-to-end through the public API (host text in pinned memory)
     # Every step copies its text from pinned host memory (H2D) and reads its counts back
@@ -478,19 +587,32 @@ def run_native(args):
         cpu = cpu_oracle_sample(spec, pats, args.cpu_seconds, len(os.sched_getaffinity(0)))
 
     # NEXT-3: a batch over a <= 4-symbol text runs PACKED on the code array packed once per
-    # call, so each pass reads n b / 8 code bytes and the text-equivalent rate can exceed the
-    # HBM peak: the kernel is ALU-bound there (compare steps), reported as such
+    # call, so each pass reads n b / 8 code bytes: the kernel is bound by the INT-ALU pipe
+    # (compare steps), not HBM.  Roofline: ALU warp-instructions of the step's search
+    # launches (instruction counts from the committed ncu capture profiles/alu_<config>.json,
+    # tools/ncu_alu.py -- counts do not depend on timing) / the live search time, against
+    # the measured ALU-pipe ceiling (profiles/alu_probe_r2.json, tools/alu_probe.py)
     roofline_pre = None
     nsym = int((hh > 0).sum())
     if nsym <= 4 and P >= 2:
         b = 1 if nsym <= 2 else 2
         code_gbs = (spec.n * b / 8 * P + spec.n) / (search_ms * 1e-3) / 1e9
+        alu = load_profile(f"alu_{cfg}.json")
+        probe = load_profile("alu_probe_r2.json")
+        work = alu.get("alu_warp_inst_per_step") if alu and alu.get("patterns") == P and \
+            alu.get("text_bytes") == spec.n and world == 1 else None
+        peak_alu = probe.get("alu_warp_inst_per_s") if probe else None
+        ach = work / (search_ms * 1e-3) if work else None
         roofline_pre = {
-            "bound": "alu", "achieved": round(achieved, 1), "unit": "GB/s (text-equivalent)", "peak": None,
-            "frac": None, "hbm_GBps_code_bytes": round(code_gbs, 1), "hbm_frac_code_bytes": round(code_gbs / peak, 4),
-            "note": f"{b}-bit code array packed once per call; each pass reads n*{b}/8 bytes; compare-bound "
-                    "(SIMDcompare steps per warp-block: profiles/compare_counters_r1.md, ncu: "
-                    "profiles/ncu_packed_c4m32_r1.txt)",
+            "bound": "alu", "achieved": ach, "peak": peak_alu, "unit": "ALU-pipe warp-instructions/s",
+            "frac": round(ach / peak_alu, 4) if ach and peak_alu else None, "traffic": None,
+            "alu_warp_inst_per_step": work, "peak_source": "profiles/alu_probe_r2.json (LOP3/SHF chains, all SMs)",
+            "work_source": f"profiles/alu_{cfg}.json (ncu smsp__inst_executed_pipe_alu.sum, search launches)",
+            "issue_active_pct_ncu": alu.get("issue_active_pct") if alu else None,
+            "alu_pipe_active_pct_ncu": alu.get("alu_pipe_active_pct") if alu else None,
+            "text_equivalent_GBps": round(achieved, 1),
+            "hbm_GBps_code_bytes": round(code_gbs, 1), "hbm_frac_code_bytes": round(code_gbs / peak, 4),
+            "note": f"{b}-bit code array packed once per call; each pass reads n*{b}/8 bytes; compare-bound",
             "kernel": "search_kernel (PACKED-PRE count)", "avg_launch_us": round(search_ms * 1e3 / P, 2),
         }
 
@@ -509,7 +631,7 @@ def run_native(args):
         "warmup": args.warmup,
         "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if strong else "weak",
         "vs_baseline": None,
         "dtype": "u8",
         "data": "synthetic",
@@ -518,7 +640,16 @@ def run_native(args):
             "patterns": P, "lengths": lens, "parallelism": f"text-shard x{world}",
             "l2": "inputs larger than L2 (256 MiB/GPU vs 126 MB); TMA loads use L2 evict_first",
             "step": "hist + per-pattern order + batched count launches (each pattern a full pass) (+ all_reduce)",
+            "halo_bytes": shard.halo,
         },
+        "collective": None if world == 1 else {
+            "kind": "NVLS multimem.red (count_sharded_fused)" if fused else "NCCL all_reduce int64[P] (SUM)",
+            "fused_requested": bool(args.fused), "multicast_available": fused,
+            "ms_per_step": round(coll_ms, 4), "search_ms_per_step": round(search_ms, 4),
+            "value_without_collective": round(bytes_per_step / ((ms_per_step - coll_ms) * 1e-3) / 1e9, 2),
+            "nccl_init": nccl_init_lines(nccl_log) if nccl_log else [],
+        },
+        "parity": parity,
         "gpu_launches": int(launches),
         "roofline": roofline_pre if roofline_pre else {
             "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -550,6 +681,7 @@ def run_native(args):
 
 def main():
     args = parse()
+    maybe_relaunch(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -30,7 +30,10 @@
  *     and its order are packed into kernel parameters at launch).
  *   - The caller owns every buffer; the library keeps no pointer after the
  *     call returns (async calls: after the enqueued work completes).
- *   - Scratch comes from the stream-ordered allocator (cudaMallocAsync).
+ *   - Scratch comes from the library's own stream-ordered memory pool per
+ *     device (cudaMemPoolCreate; freed blocks stay cached up to
+ *     SMGPU_POOL_KEEP_BYTES, default 1 GiB); the device's default pool is not
+ *     touched.
  *   - stream: a cudaStream_t passed as void*; NULL means cudaStreamPerThread.
  *
  * Errors: every call except sm_count returns sm_status and records it (with a
@@ -74,9 +77,17 @@ typedef enum sm_status {
  *     small alphabets / periodic text.
  *  SM_STRATEGY_PACKED: BLOCK on b-bit codes (b = 1 or 2) of the text bytes,
  *     code(x) = (x >> s) & (2^b - 1) with s chosen so that the code is injective
- *     on the symbols present in t (from hist: it MUST be t's histogram); needs
- *     <= 4 text symbols and every pattern symbol present in t, else SM_EINVAL.
+ *     on the symbols present in t according to hist; needs <= 4 symbols in hist
+ *     and every pattern symbol present in hist, else SM_EINVAL.
  *     For DNA / binary text (compare-bound regime).
+ *     A caller histogram is ADVISORY (frequencies "computed in
+ *     advance from some relevant corpus"): it steers order and strategy, never
+ *     the result.  When a caller hist would select PACKED, counting packs the
+ *     text once on the device and checks there that every byte of t is one of
+ *     hist's symbols; if one is not, the PACKED launches yield on the device to
+ *     byte-compare launches of the same patterns (BLOCK / PAIR / FILTER), with
+ *     no host synchronisation.  Reporting instead takes order and strategy from
+ *     t's own device histogram whenever a caller hist would allow PACKED.
  *  SM_STRATEGY_PAIR: FILTER with the rarest-two-symbol chunk test: a 16-byte
  *     chunk is queued only if one of its alignments matches pi(1) AND pi(2)
  *     (m >= 2; m = 1 runs FILTER).  Best when pi(1) is too frequent for
@@ -129,8 +140,9 @@ sm_status sm_order_from_histogram(const uint64_t* hist, const uint8_t* p, size_t
 
 /* Enqueue the count of p in t on `stream`; the result lands in *d_count
  * (DEVICE u64, overwritten).
- *   hist     host u64[256] symbol counts of t (for order and strategy);
- *            NULL -> computed on the device (synchronises `stream`).
+ *   hist     host u64[256] symbol frequencies for order and strategy (t's
+ *            histogram, or another corpus's: advisory, see SM_STRATEGY_PACKED);
+ *            NULL -> t's histogram computed on the device (synchronises `stream`).
  *   order    host u32[m] comparison order (any permutation of 0..m-1);
  *            NULL -> rarest-first from hist.
  *   peel     peeling factor r >= 1 (clamped to m, reading R9); 0 -> auto.

@@ -23,6 +23,7 @@ from __future__ import annotations
 import ctypes
 import os
 import subprocess
+import threading
 from typing import Sequence
 
 import numpy as np
@@ -31,6 +32,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 _lib = None
+_lock = threading.Lock()
 
 _u8p = ctypes.POINTER(ctypes.c_uint8)
 _u32p = ctypes.POINTER(ctypes.c_uint32)
@@ -40,13 +42,21 @@ _u64p = ctypes.POINTER(ctypes.c_uint64)
 def build(force: bool = False) -> str:
     """Compile oracle.c with gcc (plain -O2, no vectorisation flags)."""
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
-        tmp = _LIB_PATH + f".tmp{os.getpid()}"
+        tmp = _LIB_PATH + f".tmp{os.getpid()}.{threading.get_ident()}"
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-shared", "-fPIC", "-o", tmp, _SRC])
         os.replace(tmp, _LIB_PATH)
     return _LIB_PATH
 
 
 def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:  # first use from several threads at once (tools/make_golden.py): build once
+        return _load_locked()
+
+
+def _load_locked():
     global _lib
     if _lib is None:
         build()

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -258,50 +259,91 @@ int text_code_bits(const uint64_t* hist, uint32_t* shift) {
 }
 
 
-// The stream-ordered allocator returns freed blocks to the driver at every
-// synchronisation by default; keep them cached so per-call report scratch costs no
-// remapping (once per device).
-void keep_pool_cached() {
+// Per-call scratch (report staging, code arrays, count cells) comes from the library's
+// own stream-ordered pool per device -- not the device's default pool, whose attributes
+// belong to the process.  Freed blocks stay cached up to SMGPU_POOL_KEEP_BYTES (default
+// 1 GiB) across synchronisations, so repeated calls cost no remapping; anything above is
+// returned to the driver at the next synchronisation.
+uint64_t pool_keep_bytes() {
+  static const uint64_t v = [] {
+    const char* e = std::getenv("SMGPU_POOL_KEEP_BYTES");
+    return e ? (uint64_t)std::strtoull(e, nullptr, 10) : (1ull << 30);
+  }();
+  return v;
+}
+
+cudaError_t pool_alloc(void** ptr, size_t bytes, cudaStream_t st) {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
-  static bool done[64] = {false};
-  if (done[dev]) return;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaMallocAsync(ptr, bytes, st);
+  static cudaMemPool_t pools[64] = {};
+  static std::mutex mu;
   cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (!pools[dev]) {
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.handleTypes = cudaMemHandleTypeNone;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      cudaMemPool_t p;
+      e = cudaMemPoolCreate(&p, &props);
+      if (e != cudaSuccess) return e;
+      uint64_t thr = pool_keep_bytes();
+      cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr);
+      pools[dev] = p;
+    }
+    pool = pools[dev];
   }
-  done[dev] = true;
+  return cudaMallocFromPoolAsync(ptr, bytes, pool, st);
 }
 
 // NEXT-3: for a batch of >= 2 patterns over a <= 4-symbol text, pack the text once
 // into its code array and run the PACKED patterns on it (kPackedBPre).  Returns the
 // array (stream-ordered allocation, caller frees) or nullptr; *b_out = code bits.
-uint8_t* prepack_text(const uint64_t* hist, const uint8_t* t, size_t n, size_t P, cudaStream_t st, int* b_out,
-                      cudaError_t* err) {
+// guard (hist is the caller's, not computed here from t -- PAPER.md:113 allows corpus
+// frequencies, which need not be t's): packs for any P, and the pack kernel also checks
+// that every text byte is one of the symbols the code field was chosen for, setting the
+// device flag *flag_out (u32 after the array) otherwise.  The PACKED launches on the
+// array then run guarded (kGuardClear) next to a byte-compare fallback (kGuardSet), so
+// a histogram that is not t's can change the speed but never the result.
+uint8_t* prepack_text(const uint64_t* hist, const uint8_t* t, size_t n, size_t P, bool guard, cudaStream_t st,
+                      int* b_out, uint32_t** flag_out, cudaError_t* err) {
   *err = cudaSuccess;
   *b_out = 0;
-  if (!tunables().prepack || P < std::max<uint32_t>(1u, tunables().prepack_min_p) || n == 0) return nullptr;
+  *flag_out = nullptr;
+  if (!tunables().prepack || (!guard && P < std::max<uint32_t>(1u, tunables().prepack_min_p)) || n == 0 || P == 0)
+    return nullptr;
   uint32_t shift = 0;
   const int b = text_code_bits(hist, &shift);
   if (!b) return nullptr;
+  uint32_t syms = 0;  // the (<= 4) symbols present per hist, the first repeated to fill 4 bytes
+  int ns = 0;
+  for (int c = 0; c < 256; ++c)
+    if (hist[c]) syms |= (uint32_t)c << (8 * ns++);
+  for (int i = ns; i < 4; ++i) syms |= (syms & 0xFFu) << (8 * i);
   const uintptr_t tp = reinterpret_cast<uintptr_t>(t);
   const uint64_t delta = tp & 15;
   // alignments covered: every tile of every pattern plus the largest post region
   const uint64_t X = ((delta + n + 32767) / 32768 + 1) * 32768 + 8192;
   const uint64_t bytes = ((X * (uint64_t)b / 8) + 15) & ~15ull;
-  keep_pool_cached();  // per-call scratch: no remapping from the second call on
   uint8_t* codes = nullptr;
-  *err = cudaMallocAsync(reinterpret_cast<void**>(&codes), bytes, st);
+  *err = pool_alloc(reinterpret_cast<void**>(&codes), bytes + (guard ? 16 : 0), st);
   if (*err != cudaSuccess) return nullptr;
-  *err = launch_pack_text(reinterpret_cast<const uint8_t*>(tp & ~(uintptr_t)15), delta, n, shift, b, codes, bytes,
-                          num_sms(), st);
+  uint32_t* flag = guard ? reinterpret_cast<uint32_t*>(codes + bytes) : nullptr;
+  if (flag) *err = cudaMemsetAsync(flag, 0, 4, st);
+  if (*err == cudaSuccess)
+    *err = launch_pack_text(reinterpret_cast<const uint8_t*>(tp & ~(uintptr_t)15), delta, n, shift, b, codes, bytes,
+                            syms, flag, num_sms(), st);
   if (*err != cudaSuccess) {
     cudaFreeAsync(codes, st);
     return nullptr;
   }
   ++g_launches;
   *b_out = b;
+  *flag_out = flag;
   return codes;
 }
 
@@ -336,8 +378,12 @@ TextInfo text_info(const uint64_t* hist, uint64_t n, size_t P = 1) {
   return t;
 }
 
+// allow_packed = false: PACKED is never chosen (AUTO keeps the byte strategy; a forced
+// SM_STRATEGY_PACKED runs BLOCK, the same comparisons on bytes) -- for a caller histogram
+// whose code field the device cannot check, and for the guarded fallback launches.
 sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist, const uint32_t* order,
-                    uint32_t peel, int strategy, Plan& pl, const TextInfo* tinfo = nullptr) {
+                    uint32_t peel, int strategy, Plan& pl, const TextInfo* tinfo = nullptr,
+                    bool allow_packed = true) {
   if (strategy < SM_STRATEGY_AUTO || strategy > SM_STRATEGY_PAIR) return fail(SM_EINVAL, "bad strategy");
   TextInfo local;
   if (!tinfo) {
@@ -374,7 +420,7 @@ sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist
       // m = 2: PAIR's pair test, taken per byte, is the match itself (one pass, no queue,
       // no phase B: search_impl.cuh filter_tile_q), so it replaces BLOCK at any density
       strategy = m == 2 ? kPair : kBlock;
-      if (tunables().auto_packed) {  // small text alphabet: compare b-bit codes
+      if (tunables().auto_packed && allow_packed) {  // small text alphabet: compare b-bit codes
         const int pk = packed();
         if (pk) strategy = pk;
       }
@@ -390,6 +436,7 @@ sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist
     if (!strategy)
       return fail(SM_EINVAL, "SM_STRATEGY_PACKED needs <= 4 text symbols separable by a 1- or 2-bit field and "
                              "every pattern symbol present in the text");
+    if (!allow_packed) strategy = kBlock;
   }
   pl.strategy = strategy;
   if (peel == 0) {
@@ -427,7 +474,7 @@ sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist
 
 sm_status host_hist(const uint8_t* t, size_t n, cudaStream_t st, uint64_t* out) {
   uint64_t* d = nullptr;
-  SM_CUDA_TRY(cudaMallocAsync(&d, 256 * sizeof(uint64_t), st), "cudaMallocAsync(hist)");
+  SM_CUDA_TRY(pool_alloc(reinterpret_cast<void**>(&d), 256 * sizeof(uint64_t), st), "pool_alloc(hist)");
   cudaError_t e = launch_hist(t, n, d, num_sms(), st);
   if (e == cudaSuccess) {
     ++g_launches;
@@ -590,77 +637,47 @@ void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_
   }
 }
 
-sm_status prepare(const uint8_t* p, size_t m, const uint8_t* t, size_t n, const uint64_t* hist,
-                  const uint32_t* order, uint32_t peel, int strategy, cudaStream_t st, Plan& pl,
-                  uint64_t* hist_buf) {
-  const uint64_t* h = hist;
-  if (!h) {
-    sm_status s = host_hist(t, n, st, hist_buf);
-    if (s != SM_OK) return s;
-    h = hist_buf;
-  }
-  return make_plan(p, m, n, h, order, peel, strategy, pl);
-}
-
 sm_status launch_checked(const HostLaunch& L, cudaStream_t st, const char* what) {
   SM_CUDA_TRY(launch_search(L, st), what);
   ++g_launches;
   return SM_OK;
 }
 
-sm_status enqueue_count(const uint8_t* p, size_t m, const uint8_t* t, size_t n, const uint64_t* hist,
-                        const uint32_t* order, uint32_t peel, int strategy, uint64_t* d_count, cudaStream_t st) {
-  SM_CUDA_TRY(cudaMemsetAsync(d_count, 0, sizeof(uint64_t), st), "cudaMemsetAsync(count)");
-  if (n < m) return SM_OK;  // reading R2: zero alignments
-  Planned q{Plan(), p, m, d_count};
-  uint64_t hb[256];
-  sm_status s = prepare(p, m, t, n, hist, order, peel, strategy, st, q.pl, hb);
-  if (s != SM_OK) return s;
-  HostLaunch L;
-  build_launch({&q}, t, n, UINT64_MAX, kEpiCount, L);
-  if (use_dispatch(n, 1) && L.a.total_work < kNoItem) {
-    keep_pool_cached();
-    unsigned long long* work = nullptr;
-    SM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&work), 8, st), "cudaMallocAsync(work counter)");
-    cudaError_t e = cudaMemsetAsync(work, 0, 8, st);
-    L.a.work_ctr = work;
-    sm_status r = e == cudaSuccess ? launch_checked(L, st, "search kernel") : cuda_fail(e, "cudaMemsetAsync");
-    cudaFreeAsync(work, st);
-    return r;
-  }
-  return launch_checked(L, st, "search kernel");
-}
-
 // Counts of P patterns over one text in as few launches as the batch limits allow
 // (each launch runs every one of its patterns as a full pass over the text).
+// order / peel: the caller's comparison order and peeling factor (P == 1 only).
 sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t P, const uint8_t* t, size_t n,
                               uint64_t lim, const uint64_t* hist, int strategy, uint64_t* d_counts,
-                              cudaStream_t st) {
+                              cudaStream_t st, const uint32_t* order = nullptr, uint32_t peel = 0) {
   if (P == 0) return SM_OK;
   SM_CUDA_TRY(cudaMemsetAsync(d_counts, 0, P * sizeof(uint64_t), st), "cudaMemsetAsync(counts)");
   uint64_t hb[256];
   const uint64_t* h = hist;
+  const bool trusted = hist == nullptr;  // the histogram is computed here, from t
   if (!h) {
     sm_status s = host_hist(t, n, st, hb);
     if (s != SM_OK) return s;
     h = hb;
   }
-  // NEXT-3: a <= 4-symbol text is packed once for the whole batch
+  // NEXT-3: a <= 4-symbol text is packed once for the whole batch (on a caller histogram:
+  // for any P, with the device support check and the guarded fallback, see prepack_text)
   int cb = 0;
+  uint32_t* guard = nullptr;
   cudaError_t pe = cudaSuccess;
-  CodeArray codes{prepack_text(h, t, n, P, st, &cb, &pe), st};
+  CodeArray codes{prepack_text(h, t, n, P, !trusted, st, &cb, &guard, &pe), st};
   if (pe != cudaSuccess) return cuda_fail(pe, "prepack");
+  const bool allow_packed = trusted || codes.p != nullptr;
   // plan and launch as we go: a batch is launched as soon as it is full, so the GPU
   // starts on the first patterns while the host still orders the later ones
   const TextInfo tinfo = text_info(h, n, P);
   // counter-dispatched work items for long calls: one zeroed counter per launch
-  // (a call makes at most P + 7 launches: every flush holds >= 1 pattern)
+  // (a call makes at most 2 (P + 7) launches: every flush holds >= 1 pattern, and a
+  // guarded PACKED launch has a fallback launch)
   unsigned long long* work = nullptr;
   size_t nwork = 0, used_work = 0;
   if (use_dispatch(n, P)) {
-    keep_pool_cached();
-    nwork = P + 8;
-    SM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&work), nwork * 8, st), "cudaMallocAsync(work counters)");
+    nwork = 2 * (P + 8);
+    SM_CUDA_TRY(pool_alloc(reinterpret_cast<void**>(&work), nwork * 8, st), "pool_alloc(work counters)");
     cudaError_t e = cudaMemsetAsync(work, 0, nwork * 8, st);
     if (e != cudaSuccess) {
       cudaFreeAsync(work, st);
@@ -674,40 +691,66 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
       if (p) cudaFreeAsync(p, st);
     }
   } free_work{work, st};
-  std::vector<Planned> plans(P);
+  std::vector<Planned> plans(P), fallback(guard ? P : 0);
   constexpr int kStrategies = 8;                  // index = strategy value (1..7)
-  std::vector<const Planned*> batch[kStrategies];
-  size_t words[kStrategies] = {0, 0, 0, 0, 0, 0, 0, 0};
-  auto flush = [&](int strat) -> sm_status {
-    if (batch[strat].empty()) return SM_OK;
+  std::vector<const Planned*> batch[2][kStrategies];  // [0]: plans, [1]: guarded fallbacks
+  size_t words[2][kStrategies] = {};
+  auto flush = [&](int fb, int strat) -> sm_status {
+    if (batch[fb][strat].empty()) return SM_OK;
     HostLaunch L;
-    build_launch(batch[strat], t, n, lim, kEpiCount, L);
+    build_launch(batch[fb][strat], t, n, lim, kEpiCount, L);
     L.a.codes = codes.p;
+    if (guard && (fb || is_prepacked(strat))) {
+      L.a.guard = guard;
+      L.a.guard_mode = fb ? kGuardSet : kGuardClear;
+    }
     if (work && used_work < nwork && L.a.total_work < kNoItem) L.a.work_ctr = work + used_work++;
-    batch[strat].clear();
-    words[strat] = 0;
-    return launch_checked(L, st, "search kernel (batch)");
+    batch[fb][strat].clear();
+    words[fb][strat] = 0;
+    return launch_checked(L, st, fb ? "search kernel (guarded fallback)" : "search kernel (batch)");
+  };
+  auto add = [&](int fb, const Planned& q) -> sm_status {
+    const int k = q.pl.strategy;
+    if (batch[fb][k].size() == (size_t)kMaxBatch || words[fb][k] + q.m > (size_t)kBatchTableWords) {
+      sm_status s = flush(fb, k);
+      if (s != SM_OK) return s;
+    }
+    batch[fb][k].push_back(&q);
+    words[fb][k] += q.m;
+    return SM_OK;
   };
   for (size_t i = 0; i < P; ++i) {
     if (n < ms[i] || lim == 0) continue;  // count stays 0
     Planned& q = plans[i];
     q = Planned{Plan(), ps[i], ms[i], d_counts + i};
-    sm_status s = make_plan(ps[i], ms[i], n, h, nullptr, 0, strategy, q.pl, &tinfo);
+    sm_status s = make_plan(ps[i], ms[i], n, h, P == 1 ? order : nullptr, P == 1 ? peel : 0, strategy, q.pl,
+                            &tinfo, allow_packed);
     if (s != SM_OK) return s;
     use_codes(codes, cb, q.pl);
-    const int k = q.pl.strategy;
-    if (batch[k].size() == (size_t)kMaxBatch || words[k] + q.m > (size_t)kBatchTableWords) {
-      s = flush(k);
+    if (guard && is_prepacked(q.pl.strategy)) {  // its byte-compare twin, run only if the check fails
+      Planned& f = fallback[i];
+      f = Planned{Plan(), ps[i], ms[i], d_counts + i};
+      s = make_plan(ps[i], ms[i], n, h, P == 1 ? order : nullptr, P == 1 ? peel : 0, strategy, f.pl, &tinfo,
+                    false);
+      if (s == SM_OK) s = add(1, f);
       if (s != SM_OK) return s;
     }
-    batch[k].push_back(&q);
-    words[k] += q.m;
-  }
-  for (int k = 1; k < kStrategies; ++k) {
-    sm_status s = flush(k);
+    s = add(0, q);
     if (s != SM_OK) return s;
   }
+  for (int fb = 0; fb < 2; ++fb)
+    for (int k = 1; k < kStrategies; ++k) {
+      sm_status s = flush(fb, k);
+      if (s != SM_OK) return s;
+    }
   return SM_OK;
+}
+
+sm_status enqueue_count(const uint8_t* p, size_t m, const uint8_t* t, size_t n, const uint64_t* hist,
+                        const uint32_t* order, uint32_t peel, int strategy, uint64_t* d_count, cudaStream_t st) {
+  const uint8_t* ps[1] = {p};
+  const size_t ms[1] = {m};
+  return enqueue_count_batch(ps, ms, 1, t, n, UINT64_MAX, hist, strategy, d_count, st, order, peel);
 }
 
 // Staging pool of the reporting pass (bytes).  Records: at most 16 B per reported
@@ -749,14 +792,20 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
   SM_CUDA_TRY(cudaMemsetAsync(d_counts, 0, P * sizeof(uint64_t), st), "cudaMemsetAsync(counts)");
   uint64_t hb[256];
   const uint64_t* h = hist;
-  if (!h) {
+  uint32_t sh_unused = 0;
+  // PACKED is exact only on a code field injective on t's own symbols: when a caller
+  // histogram (frequencies may come from another corpus) would select it,
+  // reporting takes its strategy and order from t's device histogram instead
+  const bool may_pack = strategy == SM_STRATEGY_PACKED || (strategy == SM_STRATEGY_AUTO && tunables().auto_packed);
+  if (!h || (may_pack && text_code_bits(h, &sh_unused) != 0)) {
     sm_status s = host_hist(t, n, st, hb);
     if (s != SM_OK) return s;
     h = hb;
   }
   int cb = 0;
+  uint32_t* no_guard = nullptr;
   cudaError_t pe = cudaSuccess;
-  CodeArray codes{prepack_text(h, t, n, P, st, &cb, &pe), st};
+  CodeArray codes{prepack_text(h, t, n, P, false, st, &cb, &no_guard, &pe), st};
   if (pe != cudaSuccess) return cuda_fail(pe, "prepack");
   const TextInfo tinfo = text_info(h, n, P);
   std::vector<Planned> plans;
@@ -815,8 +864,7 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
       slot[i]->item_base = items;
       items += slot[i]->ntiles;
     }
-  if (items >= (1ull << 32)) return fail(SM_EINVAL, "report: more than 2^32 (pattern, tile) work items in one call");
-  keep_pool_cached();
+  if (items >= (1ull << 31)) return fail(SM_EINVAL, "report: 2^31 or more (pattern, tile) work items in one call");
   size_t temp_bytes = 0;
   SM_CUDA_TRY(exclusive_scan_wc(nullptr, nullptr, items, nullptr, &temp_bytes, st), "scan sizing");
   auto al = [](uint64_t b) { return (b + 255) & ~255ull; };
@@ -825,9 +873,9 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
                  ovf_b = al(items * 4), ctr_b = al(16 + nL * 12), temp_b = al(temp_bytes),
                  stage_b = stage_pool_bytes(cap, items, nL);
   uint8_t* scratch = nullptr;
-  SM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+  SM_CUDA_TRY(pool_alloc(reinterpret_cast<void**>(&scratch),
                               wc_b + bits_b + ctr_b + offs_b + ovf_b + temp_b + stage_b, st),
-              "cudaMallocAsync(report scratch)");
+              "pool_alloc(report scratch)");
   uint8_t* q = scratch;  // zero-initialised part first: wc, ovf_bits, counters
   uint16_t* wc = reinterpret_cast<uint16_t*>(q); q += wc_b;
   uint32_t* ovf_bits = reinterpret_cast<uint32_t*>(q); q += bits_b;
@@ -841,6 +889,9 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
   void* temp = q; q += temp_b;
   uint8_t* stage = q;
   cudaError_t e = cudaMemsetAsync(scratch, 0, wc_b + bits_b + ctr_b, st);
+  // whole chunks only: every chunk a warp claims can hold the largest record plus its
+  // terminator, so no claimed chunk is ever left without a terminator header
+  const uint64_t stage_cap16 = stage_b / 16 / kStageChunk * kStageChunk;
   uint64_t ovf_at = 0;
   for (size_t li = 0; li < Ls.size(); ++li) {  // pass 1: per-warp counts + staged records
     if (e != cudaSuccess) break;
@@ -848,7 +899,7 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
     L.a.wc = wc;
     L.a.stage = stage;
     L.a.stage_used = stage_used;
-    L.a.stage_cap16 = stage_b / 16;
+    L.a.stage_cap16 = stage_cap16;
     L.a.ovf_bits = ovf_bits;
     L.a.ovf_items = ovf_items + ovf_at;  // this launch's overflow queue (capacity: its items)
     L.a.ovf_n = ovf_n + li;
@@ -863,7 +914,7 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
     if (e == cudaSuccess) g_launches += 1;
   }
   if (e == cudaSuccess) {
-    e = launch_stage_expand(stage, stage_used, stage_b / 16, wc, offsets, pos, cap, expand_work, num_sms(), st);
+    e = launch_stage_expand(stage, stage_used, stage_cap16, wc, offsets, pos, cap, expand_work, num_sms(), st);
     if (e == cudaSuccess) ++g_launches;
   }
   for (size_t li = 0; li < Ls.size(); ++li) {  // overflow pass (CTAs exit at once when the queue is empty)
@@ -904,9 +955,9 @@ uint64_t sm_count(const uint8_t* p, size_t m, const uint8_t* t, size_t n) {
   if (n < m) return 0;
   cudaStream_t st = cudaStreamPerThread;
   uint64_t* d = nullptr;
-  cudaError_t e = cudaMallocAsync(&d, sizeof(uint64_t), st);
+  cudaError_t e = pool_alloc(reinterpret_cast<void**>(&d), sizeof(uint64_t), st);
   if (e != cudaSuccess) {
-    cuda_fail(e, "cudaMallocAsync(count)");
+    cuda_fail(e, "pool_alloc(count)");
     return SM_COUNT_ERROR;
   }
   sm_status s = enqueue_count(p, m, t, n, nullptr, nullptr, 0, SM_STRATEGY_AUTO, d, st);
@@ -938,7 +989,7 @@ sm_status sm_report(const uint8_t* p, size_t m, const uint8_t* t, size_t n, uint
   if (n < m) return SM_OK;
   cudaStream_t st = cudaStreamPerThread;
   uint64_t* d = nullptr;
-  SM_CUDA_TRY(cudaMallocAsync(&d, sizeof(uint64_t), st), "cudaMallocAsync(count)");
+  SM_CUDA_TRY(pool_alloc(reinterpret_cast<void**>(&d), sizeof(uint64_t), st), "pool_alloc(count)");
   s = enqueue_report(p, m, t, n, nullptr, nullptr, 0, SM_STRATEGY_AUTO, pos, cap, d, st);
   uint64_t h = 0;
   cudaError_t e = cudaSuccess;
@@ -1041,7 +1092,7 @@ sm_status sm_count_batch_multicast(const uint8_t* const* p, const size_t* m, siz
   if (reinterpret_cast<uintptr_t>(mc_counts) & 7u) return fail(SM_EINVAL, "mc_counts must be 8-byte aligned");
   cudaStream_t st = as_stream(stream);
   uint64_t* local = nullptr;  // this rank's counts, then one multimem.red per pattern
-  SM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&local), P * sizeof(uint64_t), st), "cudaMallocAsync(counts)");
+  SM_CUDA_TRY(pool_alloc(reinterpret_cast<void**>(&local), P * sizeof(uint64_t), st), "pool_alloc(counts)");
   sm_status s = enqueue_count_batch(p, m, P, t, n, (uint64_t)max_alignments, hist, strategy, local, st);
   if (s == SM_OK) {
     cudaError_t e = launch_nvls_add(local, mc_counts, P, st);

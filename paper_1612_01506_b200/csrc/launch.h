@@ -34,9 +34,11 @@ cudaError_t launch_stage_expand(const uint8_t* stage, const unsigned long long* 
                                 unsigned long long* work /* zeroed chunk counter */, int num_sms, cudaStream_t st);
 
 // NEXT-3: the text's b-bit code array (code(x) = (x >> shift) & (2^b - 1)), base-relative
-// alignment x <-> bits [b x, b x + b); code_bytes (multiple of 16) of it, zero past the text
+// alignment x <-> bits [b x, b x + b); code_bytes (multiple of 16) of it, zero past the text.
+// bad != nullptr: also sets *bad (device u32, zeroed by the caller) if some text byte is
+// not one of the four bytes of syms (the symbols the code field was chosen for).
 cudaError_t launch_pack_text(const uint8_t* base, uint64_t delta, uint64_t n, uint32_t shift, int b, uint8_t* codes,
-                             uint64_t code_bytes, int num_sms, cudaStream_t st);
+                             uint64_t code_bytes, uint32_t syms, uint32_t* bad, int num_sms, cudaStream_t st);
 
 // NEXT-4: mc[i] += local[i] through an NVLink multicast address (multimem.red)
 cudaError_t launch_nvls_add(const uint64_t* local, uint64_t* mc, uint64_t P, cudaStream_t st);

@@ -118,7 +118,12 @@ struct LaunchArgs {
   unsigned long long* ctr;   // instrumented build (SMGPU_COUNTERS) only: device u64[kCounters], else unused
   unsigned long long* work_ctr;  // count / stage: non-null = work items are dispatched from this zeroed
                                  // counter (the producer fetches, the consumers read the stage's item)
+  const uint32_t* guard;     // device flag set by pack_text_kernel when a text byte lies outside the symbol
+                             // set the code field was chosen for (a caller histogram that is not t's)
+  uint32_t guard_mode;       // 0: always run; kGuardClear: run only if *guard == 0 (PACKED on a caller
+                             // histogram); kGuardSet: run only if *guard != 0 (its byte-compare fallback)
 };
+constexpr uint32_t kGuardClear = 1, kGuardSet = 2;
 
 // Compare-step counters of the instrumented build (libsmgpu_counters.so, NEXT-2):
 enum Counter : int {

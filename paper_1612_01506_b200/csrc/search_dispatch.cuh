@@ -12,11 +12,14 @@ namespace {
 template <int STRAT, int EPI, int CAP, int CPL>
 cudaError_t launch_one(const HostLaunch& L, cudaStream_t st) {
   auto kfn = search_kernel<STRAT, EPI, CAP, CPL>;
-  static bool attr_done = false;  // benign race: idempotent attribute set
-  if (!attr_done) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  // the attribute belongs to the device's context: set once per (kernel, device)
+  static bool attr_done[64] = {};  // benign race: idempotent attribute set
+  if (!attr_done[dev]) {
     cudaError_t err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (err != cudaSuccess) return err;
-    attr_done = true;
+    attr_done[dev] = true;
   }
   // persistent grid: never more CTAs than can be resident at once (registers or shared
   // memory may allow fewer per SM than the host's plan assumed) -- a second wave of CTAs
@@ -24,15 +27,17 @@ cudaError_t launch_one(const HostLaunch& L, cudaStream_t st) {
   int grid = L.grid;
   {
     static thread_local size_t cached_smem = ~(size_t)0;
+    static thread_local int cached_dev = -1;
     static thread_local int cached_blocks = 0;
-    if (cached_smem != L.smem) {
+    if (cached_smem != L.smem || cached_dev != dev) {
       int nb = 0;
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kfn, kThreads, L.smem) != cudaSuccess) nb = 0;
       cached_smem = L.smem;
+      cached_dev = dev;
       cached_blocks = nb;
     }
-    int dev = 0, sms = 0;
-    if (cached_blocks > 0 && cudaGetDevice(&dev) == cudaSuccess &&
+    int sms = 0;
+    if (cached_blocks > 0 &&
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0)
       grid = grid < cached_blocks * sms ? grid : cached_blocks * sms;
   }

@@ -911,7 +911,10 @@ struct StageAlloc {
       if (c >= a.stage_cap16) return ~0ull;
       next = c;
       end = c + kStageChunk < a.stage_cap16 ? c + kStageChunk : a.stage_cap16;
-      if (next + units + 1 > end) return ~0ull;  // the pool's last, partial chunk is too small
+      if (next + units + 1 > end) {  // (cannot happen: the host hands out whole chunks only)
+        reinterpret_cast<uint4*>(a.stage)[c] = make_uint4(0u, 0u, 0u, 0u);  // the chunk holds no record
+        return ~0ull;
+      }
     }
     const unsigned long long o = next;
     next += units;  // the terminator slot is reused by the next record
@@ -1020,6 +1023,10 @@ __global__ void __launch_bounds__(kThreads,
     search_kernel(const __grid_constant__ LaunchParams<CAP> P) {
   extern __shared__ __align__(128) uint8_t smem[];
   const LaunchArgs& a = P.a;
+  if (a.guard_mode) {  // PACKED on a caller histogram, or its fallback: exactly one of the pair runs
+    const uint32_t g = *reinterpret_cast<const volatile uint32_t*>(a.guard);
+    if ((g != 0u) != (a.guard_mode == kGuardSet)) return;
+  }
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + kMaxStages;
   uint32_t* s_wt = reinterpret_cast<uint32_t*>(smem + kWarpTotOff);  // [2][W]

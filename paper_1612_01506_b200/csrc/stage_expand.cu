@@ -219,11 +219,13 @@ cudaError_t launch_stage_expand(const uint8_t* stage, const unsigned long long* 
                                 unsigned long long* work, int num_sms, cudaStream_t st) {
   if (stage_cap16 == 0) return cudaSuccess;
   const size_t smem = (size_t)kExpandWarps * kWarpSmem;
-  static bool attr = false;  // benign race: idempotent
-  if (!attr) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  static bool attr[64] = {};  // per device context; benign race: idempotent
+  if (!attr[dev]) {
     cudaError_t e = cudaFuncSetAttribute(stage_expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr[dev] = true;
   }
   const uint64_t max_chunks = (stage_cap16 + kStageChunk - 1) / kStageChunk;
   const uint64_t want = (max_chunks + kExpandWarps - 1) / kExpandWarps;

@@ -142,6 +142,8 @@ def count_sharded_fused(patterns, shard_text, shard: Shard, hist, mc: "Multicast
     if not mc.available:
         return count_sharded(patterns, shard_text, shard, hist, group=group, strategy=strategy)
     pb = patterns if isinstance(patterns, sm.PatternBatch) else sm.PatternBatch(patterns)
+    if pb.P > mc.P:
+        raise ValueError(f"{pb.P} patterns but the multicast count buffer holds {mc.P}")
     shard.view_len(max((len(p) for p in pb.data), default=1))  # halo check
     mc.local.zero_()
     torch.cuda.synchronize()

@@ -12,9 +12,10 @@ torch.cuda.set_device(0)
 print("library:", sm.load_library()._name, "SMGPU_STAGE_BYTES:", os.environ.get("SMGPU_STAGE_BYTES"))
 rng = np.random.default_rng(2024)
 fails = 0
+SMALL = os.environ.get("SMGPU_WORKLOAD_SMALL") == "1"  # compute-sanitizer runs (tools/sanitize.sh)
 for alpha in (b"ACGT", b"\x00\x01", bytes(range(32, 127)), b"a"):
     syms = np.frombuffer(alpha, dtype=np.uint8)
-    for n in (5, 31, 4100, 70003):
+    for n in ((5, 31, 4100) if SMALL else (5, 31, 4100, 70003)):
         a = syms[rng.integers(0, syms.size, n)]
         h = oracle.hist(a)
         for off in (0, 3, 15):
@@ -44,6 +45,32 @@ for alpha in (b"ACGT", b"\x00\x01", bytes(range(32, 127)), b"a"):
                 got, tot = sm.sm_report(p, t)
                 fails += tot != oracle.naive_count(p, a) or not np.array_equal(
                     got.cpu().numpy().astype(np.uint64), oracle.naive_report(p, a).astype(np.uint64))
+# dense reports that fill the staging pool (every alignment matches): with a small
+# SMGPU_STAGE_BYTES the tiles split between staged records and the overflow pass
+for n in ((70003,) if SMALL else (70003, 300001)):
+    a = np.full(n, ord("a"), dtype=np.uint8)
+    t = torch.from_numpy(a).cuda()
+    pats = [b"a", b"aa", b"a" * 17]
+    want = [n - len(p) + 1 for p in pats]
+    for cap in (sum(want), 10, 4000):
+        pos = torch.zeros(cap, dtype=torch.int64, device="cuda")
+        d2 = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
+        sm.sm_report_batch(pats, t, pos, d2)
+        fails += d2.cpu().tolist() != want
+        wp = np.concatenate([np.arange(w, dtype=np.uint64) for w in want])[:cap]
+        fails += not np.array_equal(pos.cpu().numpy().astype(np.uint64), wp)
+# an advisory (wrong) caller histogram: ACGT-only for a text with 'N' bytes
+a = np.frombuffer(b"ACGT", dtype=np.uint8)[rng.integers(0, 4, 9000)].copy()
+a[::97] = ord("N")
+h = np.zeros(256, dtype=np.uint64)
+h[list(b"ACGT")] = 1
+t = torch.from_numpy(a).cuda()
+pats = [b"G", b"GN", b"AGG", a[50:70].tobytes()]
+for strat in (0, 3):
+    sel = [p for p in pats if strat == 0 or b"N" not in p]
+    d = torch.zeros(len(sel), dtype=torch.int64, device="cuda")
+    sm.sm_count_batch(sel, t, d, hist=h, strategy=strat)
+    fails += d.cpu().tolist() != [oracle.naive_count(p, a) for p in sel]
 torch.cuda.synchronize()
 print("sanitize workload done, mismatches:", fails)
 sys.exit(1 if fails else 0)

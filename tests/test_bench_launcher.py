@@ -1,0 +1,82 @@
+"""bench.py's multi-GPU launch contract on the host (no GPU here):
+
+* `bench.py --gpus N` started as a plain process re-executes itself under
+  torch.distributed.run with N ranks on 127.0.0.1 -- and refuses (exit 2) when fewer
+  than N GPUs are visible, instead of silently measuring one GPU;
+* a rank started by a launcher checks WORLD_SIZE against --gpus;
+* the strong-scaling config (c5) keeps the total text fixed while the weak ones grow.
+"""
+import os
+import subprocess
+import sys
+import types
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+def test_refuses_more_gpus_than_visible():
+    env = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        env.pop(k, None)
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 2, r.stderr[-2000:]
+    assert "refusing" in r.stderr
+    assert r.stdout.strip() == ""   # no JSON line: nothing was measured
+
+
+def test_relaunch_command(monkeypatch):
+    import torch
+    calls = []
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(torch.cuda, "device_count", lambda: 8)
+    monkeypatch.setattr(bench.subprocess, "call", lambda cmd: calls.append(cmd) or 0)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "5", "--config", "c5"])
+    args = bench.parse()
+    with pytest.raises(SystemExit) as e:
+        bench.maybe_relaunch(args)
+    assert e.value.code == 0
+    (cmd,) = calls
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd
+    assert cmd[-6:] == ["--gpus", "4", "--steps", "5", "--config", "c5"]
+
+
+def test_no_relaunch_under_a_launcher_or_for_one_gpu(monkeypatch):
+    monkeypatch.setattr(bench.subprocess, "call", lambda cmd: pytest.fail("must not relaunch"))
+    monkeypatch.setenv("WORLD_SIZE", "4")
+    bench.maybe_relaunch(types.SimpleNamespace(gpus=4, impl="native"))
+    monkeypatch.delenv("WORLD_SIZE")
+    bench.maybe_relaunch(types.SimpleNamespace(gpus=1, impl="native"))
+    bench.maybe_relaunch(types.SimpleNamespace(gpus=8, impl="reference"))  # CPU arm: rank 0 only
+
+
+@pytest.mark.parametrize("world", [1, 2, 8])
+def test_strong_and_weak_workloads(world):
+    import synth
+    strong = bench.build_workload(types.SimpleNamespace(config="c5", shard_bytes=None, lengths=None, per_m=None),
+                                  0, world)
+    assert strong[0].n == 1 << 36 and len(strong[1]) == 200
+    weak = bench.build_workload(types.SimpleNamespace(config="c2", shard_bytes=1 << 20, lengths="8", per_m=2),
+                                0, world)
+    assert weak[0].n == world << 20
+    assert synth.text_spec("c5").n == 1 << 36
+
+
+def test_golden_check_catches_a_wrong_count():
+    import json
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "c1.json")))
+    want = [c["count"] for c in g["cases"]]
+    ok = bench.golden_check("c1", want, g["n"], len(want))
+    assert ok["mismatches"] == 0 and ok["count_sum"] == g["count_sum"]
+    bad = list(want)
+    bad[17] += 1
+    with pytest.raises(SystemExit):
+        bench.golden_check("c1", bad, g["n"], len(want))
+    assert bench.golden_check("c1", want, g["n"] + 1, len(want)) is None  # not the golden workload

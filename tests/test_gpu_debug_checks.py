@@ -28,6 +28,9 @@ DISPATCH_ALWAYS = {"SMGPU_DISPATCH_MIN_MB": "0", "SMGPU_DISPATCH_MIN_MB_SINGLE":
     ("debug", None, {}), ("debug", "0", {}), ("debug", "4096", {}),
     ("debug", None, DISPATCH_ALWAYS), ("debug", "4096", DISPATCH_ALWAYS),
     ("release", "0", {}), ("release", "20000", {}), ("release", None, DISPATCH_ALWAYS),
+    # a pool of 3 chunks + 20 units: (stage bytes / 16) % kStageChunk = 20 < one bitmap
+    # record, the case where a warp could claim a partial chunk it cannot use
+    ("debug", str(16 * (3 * 512 + 20)), {}), ("release", str(16 * (3 * 512 + 20)), {}),
     ("release", None, {"SMGPU_DISPATCH": "0"})])
 def test_debug_build_bounds_assertions(lib_kind, stage_bytes, extra):
     from paper_1612_01506_b200 import _build

@@ -473,3 +473,69 @@ def test_report_sharded_virtual(sm):
                 s0 = int(c[:k].sum())
                 segs.append(p[s0: s0 + int(c[k])])
             assert np.concatenate(segs).tolist() == want[k].tolist(), (G, k)
+
+
+# ------------------------------------------------------------- advisory caller histogram
+@pytest.mark.parametrize("n", [4100, 300_017])
+def test_caller_histogram_is_advisory(sm, n):
+    """PAPER.md:113 lets the frequencies come "from some relevant corpus": a caller
+    histogram that is not t's must never change a result.  DNA text with a few 'N'
+    bytes, counted with an ACGT-only histogram (which plans PACKED 2-bit codes with a
+    shift under which 'N' aliases 'G'): every entry point, AUTO and forced PACKED,
+    equals Alg. 1 (the device support check sends the PACKED launches to their
+    byte-compare fallback)."""
+    rng = np.random.default_rng(n)
+    a = np.frombuffer(b"ACGT", dtype=np.uint8)[rng.integers(0, 4, n)].copy()
+    a[rng.integers(0, n, 40)] = ord("N")
+    a[n - 1] = ord("N")                      # also in the ragged tail
+    h_acgt = np.zeros(256, dtype=np.uint64)
+    for c in b"ACGT":
+        h_acgt[c] = n // 4
+    plan = sm.sm_plan(b"GGGGGG", h_acgt)
+    assert sm.STRATEGY_NAMES[plan[0]].startswith("packed")  # the hazard is real: PACKED planned
+    for off in (0, 5):
+        t = dev(a, off)
+        pats = [b"G", b"GN", b"AG", b"ACG", b"GGGGGG", a[7:19].tobytes(), a[100:104].tobytes(), b"TTTT"]
+        want = [oracle.naive_count(p, a) for p in pats]
+        for strat in (0, 3):
+            ok_pats = [p for p in pats if all(h_acgt[c] for c in p)] if strat == 3 else pats
+            wk = [oracle.naive_count(p, a) for p in ok_pats]
+            d = torch.zeros(len(ok_pats), dtype=torch.int64, device="cuda")
+            sm.sm_count_batch(ok_pats, t, d, hist=h_acgt, strategy=strat)
+            assert d.cpu().tolist() == wk, (off, strat)
+            for p, w in zip(ok_pats, wk):
+                assert count_async(sm, p, t, hist=h_acgt, strategy=strat) == w, (p, off, strat)
+            cap = sum(wk)
+            pos = torch.zeros(max(cap, 1), dtype=torch.int64, device="cuda")
+            d2 = torch.zeros(len(ok_pats), dtype=torch.int64, device="cuda")
+            if strat == 3:  # reporting checks t's own histogram: 5 symbols, PACKED inapplicable
+                with pytest.raises(sm.SmError) as ei:
+                    sm.sm_report_batch(ok_pats, t, pos[:cap], d2, hist=h_acgt, strategy=strat)
+                assert ei.value.status == sm.SM_EINVAL
+                continue
+            sm.sm_report_batch(ok_pats, t, pos[:cap] if cap else None, d2, hist=h_acgt, strategy=strat)
+            assert d2.cpu().tolist() == wk
+            wp = np.concatenate([oracle.naive_report(p, a) for p in ok_pats])
+            assert np.array_equal(pos[:cap].cpu().numpy().astype(np.uint64), wp.astype(np.uint64))
+            for p, w in zip(ok_pats[:3], wk[:3]):
+                got, total = report_async(sm, p, t, w, hist=h_acgt, strategy=strat)
+                assert total == w and np.array_equal(got.astype(np.uint64), oracle.naive_report(p, a))
+        # the histogram of t itself still selects PACKED and agrees
+        d = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
+        sm.sm_count_batch(pats, t, d, hist=oracle.hist(a))
+        assert d.cpu().tolist() == want
+
+
+def test_caller_histogram_matching_text_keeps_packed(sm):
+    """With a caller histogram that IS t's, the guarded PACKED launches run (and the
+    fallback launches exit at once): same counts as the library-computed histogram."""
+    spec = synth.text_spec("c1")
+    a = spec.host()
+    t = dev(a)
+    pats = [a[s:s + m].tobytes() for s, m in ((10, 4), (999, 8), (5000, 16), (77777, 32), (123, 1))]
+    d = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
+    sm.sm_count_batch(pats, t, d, hist=oracle.hist(a))
+    d0 = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
+    sm.sm_count_batch(pats, t, d0)
+    want = [oracle.naive_count(p, a) for p in pats]
+    assert d.cpu().tolist() == want and d0.cpu().tolist() == want
