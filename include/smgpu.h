@@ -168,17 +168,29 @@ sm_status sm_count_batch(const uint8_t* const* p, const size_t* m, size_t P, con
                          size_t max_alignments, const uint64_t* hist, int strategy, uint64_t* d_counts,
                          void* stream);
 
-/* Multi-GPU counting without a collective call (NEXT-4): as sm_count_batch, but
- * mc_counts (u64[P]) is the NVLink MULTICAST address of a buffer bound on every
- * rank of the group (e.g. torch symmetric memory's multicast_ptr, or
- * cuMulticastCreate + cuMulticastBindMem); after the search launches a small kernel
- * adds this rank's counts with one multimem.red per pattern (NVLS reduction in the
- * switch), so when all ranks' work has completed, every rank's own copy holds the
- * sums over all ranks.  The call does NOT zero the counts: every rank
- * zeroes its copy and the group synchronises before any rank launches, and
- * synchronises again (after its stream) before reading.  Same p, m, max_alignments
- * (each rank passes its shard's owned alignments), hist and strategy as
- * sm_count_batch.  SM_EINVAL for a misaligned mc_counts. */
+/* sm_count_batch with the caller's comparison order and peeling factor per pattern
+ * (NEXT-2's fixed orders, and r sweeps, on the
+ * batched path): orders = host u32, the P orders concatenated (m[i] entries each, a
+ * permutation of 0..m[i]-1; NULL -> rarest-first from hist), peels = host u32[P]
+ * (0 or NULL -> auto).  Orders and r never change a count. */
+sm_status sm_count_batch_ordered(const uint8_t* const* p, const size_t* m, size_t P, const uint8_t* t, size_t n,
+                                 size_t max_alignments, const uint64_t* hist, const uint32_t* orders,
+                                 const uint32_t* peels, int strategy, uint64_t* d_counts, void* stream);
+
+/* Multi-GPU counting without a collective call (NEXT-4, the counting
+ * version, summed over ranks): as sm_count_batch, but mc_counts (u64[P]) is the NVLink
+ * MULTICAST address of a buffer bound on every rank of the group (e.g. torch symmetric
+ * memory's multicast_ptr, or cuMulticastCreate + cuMulticastBindMem).  The rank's
+ * counts go to library scratch, and the last CTA to finish each search launch adds
+ * its patterns' counts to mc_counts with one multimem.red each (NVLS: the switch
+ * applies the add to every rank's bound copy) -- no extra kernel, no NCCL call.  When
+ * all ranks' work has completed, every rank's own copy holds the sums over all ranks.
+ * The call does NOT zero the counts: every rank zeroes its copy and the group
+ * synchronises before any rank launches, and synchronises again (after its stream)
+ * before reading.  Same p, m, max_alignments (each rank passes its shard's owned
+ * alignments), hist and strategy as sm_count_batch.  SM_EINVAL for a misaligned
+ * mc_counts.  SMGPU_NVLS_EMULATE=1 replaces multimem.red by a plain atomic add (a
+ * unicast mc_counts: tests of the protocol on a box without multicast). */
 sm_status sm_count_batch_multicast(const uint8_t* const* p, const size_t* m, size_t P, const uint8_t* t, size_t n,
                                    size_t max_alignments, const uint64_t* hist, int strategy, uint64_t* mc_counts,
                                    void* stream);
@@ -238,7 +250,11 @@ sm_status sm_plan(const uint8_t* p, size_t m, const uint64_t* hist, const uint32
  *   out[4] FILTER chunks holding p[pi(1)]
  *   out[5] FILTER valid alignments matching pi(1) and pi(2)
  *   out[6] FILTER pattern positions compared while verifying those
- *   out[7] BLOCK/PACKED alignments per warp-block (max over launches) */
+ *   out[7] BLOCK/PACKED alignments per warp-block (max over launches)
+ *   out[8] PACKED warp-blocks finished by per-lane survivor verification
+ *   out[9] PACKED survivors of the peeled steps verified per lane there
+ *   out[10] PACKED 32-bit code words compared while verifying them
+ * (out: host u64[11]) */
 sm_status sm_counters(uint64_t* out, int reset);
 
 /* Thread-local status of the last failing call on this thread (SM_OK if none

@@ -43,11 +43,11 @@ STRATEGY_NAMES = {1: "filter", 2: "block", 3: "packed1", 4: "packed2", 5: "pair"
 
 EXPORTED_SYMBOLS = (
     "sm_count", "sm_report", "sm_symbol_order", "sm_histogram", "sm_order_from_histogram",
-    "sm_count_async", "sm_count_batch", "sm_count_batch_multicast", "sm_report_async", "sm_report_batch", "sm_heuristic_order", "sm_plan", "sm_last_error", "sm_last_error_message",
+    "sm_count_async", "sm_count_batch", "sm_count_batch_ordered", "sm_count_batch_multicast", "sm_report_async", "sm_report_batch", "sm_heuristic_order", "sm_plan", "sm_last_error", "sm_last_error_message",
     "sm_clear_error", "sm_status_string", "sm_version", "sm_launch_count", "sm_counters",
 )
 COUNTER_NAMES = ("warp_tiles", "blocks", "steps", "filter_chunks", "filter_queued", "filter_survivors",
-                 "filter_verify", "alpha_eff")
+                 "filter_verify", "alpha_eff", "sparse_blocks", "code_survivors", "code_words")
 
 
 class SmError(RuntimeError):
@@ -88,6 +88,8 @@ def load_library(path: str = LIB_PATH):
     lib.sm_count_async.argtypes = [_u8p, _sz, _u8p, _sz, _vp, _vp, ctypes.c_uint32, ctypes.c_int, _vp, _vp]
     lib.sm_count_batch.restype = ctypes.c_int
     lib.sm_count_batch.argtypes = [_vp, _vp, _sz, _u8p, _sz, _sz, _vp, ctypes.c_int, _vp, _vp]
+    lib.sm_count_batch_ordered.restype = ctypes.c_int
+    lib.sm_count_batch_ordered.argtypes = [_vp, _vp, _sz, _u8p, _sz, _sz, _vp, _vp, _vp, ctypes.c_int, _vp, _vp]
     lib.sm_count_batch_multicast.restype = ctypes.c_int
     lib.sm_count_batch_multicast.argtypes = [_vp, _vp, _sz, _u8p, _sz, _sz, _vp, ctypes.c_int, _vp, _vp]
     lib.sm_report_batch.restype = ctypes.c_int
@@ -299,6 +301,28 @@ def sm_count_batch(patterns, t, d_counts, hist=None, max_alignments: Optional[in
         _raise(s)
 
 
+def sm_count_batch_ordered(patterns, t, d_counts, orders=None, peels=None, hist=None,
+                           max_alignments: Optional[int] = None, strategy: int = SM_STRATEGY_AUTO,
+                           stream=None) -> None:
+    """sm_count_batch with per-pattern comparison orders (list of sequences, or None for
+    rarest-first) and peeling factors (list of ints, 0 = auto) -- NEXT-2 ablations."""
+    lib = load_library()
+    pb = patterns if isinstance(patterns, PatternBatch) else PatternBatch(patterns)
+    tp, n = _text(t)
+    h = _u64_host(hist)
+    o = None if orders is None else np.ascontiguousarray(np.concatenate(
+        [np.asarray(x, dtype=np.uint32) for x in orders]) if pb.P else np.zeros(0, np.uint32), dtype=np.uint32)
+    if o is not None and o.size != sum(len(d) for d in pb.data):
+        raise ValueError("orders must hold len(p) entries per pattern")
+    r = None if peels is None else np.ascontiguousarray(np.asarray(peels, dtype=np.uint32))
+    lim = (1 << 64) - 1 if max_alignments is None else int(max_alignments)
+    dptr = d_counts if isinstance(d_counts, int) else d_counts.data_ptr()
+    s = lib.sm_count_batch_ordered(ctypes.addressof(pb.ptrs), ctypes.addressof(pb.lens), pb.P, tp, n, lim,
+                                   _np_ptr(h), _np_ptr(o), _np_ptr(r), strategy, dptr, _stream(stream))
+    if s != SM_OK:
+        _raise(s)
+
+
 def sm_count_batch_multicast(patterns, t, mc_counts: int, hist=None, max_alignments: Optional[int] = None,
                              strategy: int = SM_STRATEGY_AUTO, stream=None) -> None:
     """NEXT-4: counts with the all-reduce fused into the kernel (multimem.red on the NVLink
@@ -384,7 +408,7 @@ def sm_launch_count() -> int:
 
 def sm_counters(reset: bool = False) -> dict:
     """Compare-step counters of the instrumented build (SMGPU_LIB=counters), see smgpu.h."""
-    out = np.zeros(8, dtype=np.uint64)
+    out = np.zeros(len(COUNTER_NAMES), dtype=np.uint64)
     s = load_library().sm_counters(out.ctypes.data, int(reset))
     if s:
         _raise(s)

@@ -167,6 +167,9 @@ struct Tunables {
   uint64_t dispatch_min_bytes = 64ull << 20;  // ... when the call streams at least this much text (n x P)
   uint64_t dispatch_min_bytes_single = 512ull << 20;  // single-pattern calls (the counter's memset
                                                       // costs more than it gains on short launches)
+  uint32_t packed_sparse = 128;  // PACKED: per-lane survivor verification when a warp-block has <= this many
+                                 // survivors after the peeled steps (0: Alg. 4's ordered loop always)
+  double packed_peel_surv = 32;  // PACKED + sparse: AUTO r = smallest with alpha_eff prod f <= this
 };
 
 const Tunables& tunables() {
@@ -191,6 +194,8 @@ const Tunables& tunables() {
     if (const char* e = std::getenv("SMGPU_DISPATCH_MIN_MB")) x.dispatch_min_bytes = (uint64_t)std::atoll(e) << 20;
     if (const char* e = std::getenv("SMGPU_DISPATCH_MIN_MB_SINGLE"))
       x.dispatch_min_bytes_single = (uint64_t)std::atoll(e) << 20;
+    if (const char* e = std::getenv("SMGPU_PACKED_SPARSE")) x.packed_sparse = (uint32_t)std::atoi(e);
+    if (const char* e = std::getenv("SMGPU_PACKED_PEEL_SURV")) x.packed_peel_surv = std::atof(e);
     if (x.ctas_pre < 1 || x.ctas_pre > 4) x.ctas_pre = 3;
     if (const char* e = std::getenv("SMGPU_STAGES_PRE")) x.max_stages_pre = (uint32_t)std::atoi(e);
     if (x.max_stages_pre < 2 || x.max_stages_pre > (uint32_t)kMaxStages) x.max_stages_pre = 6;
@@ -444,13 +449,19 @@ sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist
     // for r ("it is less probable that all the alpha comparisons
     // fail at the same time") at the warp's alpha_eff = 32 lanes x 16 x CPL, capped at 2048.
     double surv = std::min(32.0 * 16.0 * pl.cpl, 2048.0);
+    // PACKED with per-lane survivor verification: peel only until the warp-block's expected
+    // survivors are few enough to verify one by one (search_impl.cuh verify_code_survivors)
+    const double target = is_packed(pl.strategy) && tunables().packed_sparse ? tunables().packed_peel_surv : 0.5;
+    if (is_packed(pl.strategy)) surv = 32.0 * 16.0 * pl.cpl;
     uint32_t r = 0;
-    while (r < m && surv > 0.5) surv *= freq(r++);
+    while (r < m && surv > target) surv *= freq(r++);
     const int rb = (int)r + tunables().peel_bias;  // tuning knob (0 by default)
     peel = rb < 1 ? 1u : (uint32_t)rb;
   }
   pl.r = std::min<uint32_t>(peel, (uint32_t)m);
-  if (pl.strategy == kFilter) pl.r = 1;
+  // FILTER: pi(1) is tested per chunk, then phase B peels pi(1) and pi(2) together
+  // (filter_entry, r = 2) before the per-survivor loop
+  if (pl.strategy == kFilter) pl.r = std::min<uint32_t>(2u, (uint32_t)m);
   if (pl.strategy == kPair) {
     pl.r = 2;  // pi(1), pi(2) tested together
     // PAIR's chunk test is cheaper when pi(2)'s window is word-aligned relative to
@@ -539,6 +550,12 @@ struct Planned {
   uint64_t* count_out;
 };
 
+// kernel-parameter table entries of a planned pattern: its m (offset, symbol) pairs in
+// pi order, + its natural-order code words for PACKED
+size_t table_words(const Planned& q) {
+  return q.m + (is_packed(q.pl.strategy) ? packed_code_words((uint32_t)q.m, code_bits(q.pl.strategy)) : 0u);
+}
+
 // Build one launch over patterns `ps` (same strategy; <= kMaxBatch, table <= kTableLarge).
 // The tile is the plan's (large texts: 32 KiB); the batching loops keep a launch's
 // table <= kBatchTableWords; T is halved only if fewer than 2 stages fit.
@@ -556,12 +573,23 @@ void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_
   const bool pre = is_prepacked(L.strategy);
   const uint32_t cbits = (uint32_t)code_bits(L.strategy);
   L.a.code_shift = ps[0]->pl.code_shift;
-  for (const Planned* q : ps)
+  for (const Planned* q : ps) {
     for (size_t k = 0; k < q->m; ++k) {
       const uint32_t sym = q->p[q->pl.order[k]];
       const uint32_t v = packed ? ((sym >> L.a.code_shift) & ((1u << cbits) - 1u)) : sym;
       L.e.push_back(q->pl.order[k] | (v << 16));
     }
+    if (packed) {  // the pattern's codes in natural order (per-lane survivor verification)
+      const size_t w0 = L.e.size();
+      L.e.resize(w0 + packed_code_words((uint32_t)q->m, (int)cbits), 0u);
+      for (size_t j = 0; j < q->m; ++j) {
+        const uint32_t v = (q->p[j] >> L.a.code_shift) & ((1u << cbits) - 1u);
+        const size_t bit = j * cbits;
+        L.e[w0 + bit / 32] |= v << (bit % 32);
+      }
+    }
+  }
+  L.a.sparse_max = packed ? tunables().packed_sparse : 0u;
   L.a.npat = (uint32_t)ps.size();
   L.a.tbl_words = (uint32_t)L.e.size();
   L.a.ctr = counters_ptr();
@@ -586,7 +614,7 @@ void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_
     for (size_t i = 0; i < ps.size(); ++i) {
       const Planned& q = *ps[i];
       fill_desc(q.pl, q.p, q.m, L.a.delta, n, lim, T, L.d[i], tbl);
-      tbl += (uint32_t)q.m;
+      tbl += table_words(q);
       work += L.d[i].ntiles;
       L.d[i].work_end = work;
       L.d[i].count_out = q.count_out;
@@ -646,9 +674,14 @@ sm_status launch_checked(const HostLaunch& L, cudaStream_t st, const char* what)
 // Counts of P patterns over one text in as few launches as the batch limits allow
 // (each launch runs every one of its patterns as a full pass over the text).
 // order / peel: the caller's comparison order and peeling factor (P == 1 only).
+// orders / peels: the caller's comparison orders (concatenated, m[i] entries each) and
+// peeling factors (0 = auto), or nullptr for the rarest-first order / auto r.
+// mc / done (NEXT-4): every launch also adds its patterns' counts to mc[i] through the
+// last-CTA epilogue (search_impl.cuh nvls_epilogue); done = >= 2 (P + 8) zeroed u32.
 sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t P, const uint8_t* t, size_t n,
                               uint64_t lim, const uint64_t* hist, int strategy, uint64_t* d_counts,
-                              cudaStream_t st, const uint32_t* order = nullptr, uint32_t peel = 0) {
+                              cudaStream_t st, const uint32_t* orders = nullptr, const uint32_t* peels = nullptr,
+                              uint64_t* mc = nullptr, unsigned int* done = nullptr) {
   if (P == 0) return SM_OK;
   SM_CUDA_TRY(cudaMemsetAsync(d_counts, 0, P * sizeof(uint64_t), st), "cudaMemsetAsync(counts)");
   uint64_t hb[256];
@@ -691,6 +724,7 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
       if (p) cudaFreeAsync(p, st);
     }
   } free_work{work, st};
+  size_t used_done = 0;
   std::vector<Planned> plans(P), fallback(guard ? P : 0);
   constexpr int kStrategies = 8;                  // index = strategy value (1..7)
   std::vector<const Planned*> batch[2][kStrategies];  // [0]: plans, [1]: guarded fallbacks
@@ -705,33 +739,45 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
       L.a.guard_mode = fb ? kGuardSet : kGuardClear;
     }
     if (work && used_work < nwork && L.a.total_work < kNoItem) L.a.work_ctr = work + used_work++;
+    if (mc) {
+      static const bool emulate = [] {
+        const char* e = std::getenv("SMGPU_NVLS_EMULATE");
+        return e && std::atoi(e) != 0;
+      }();
+      L.a.mc_base = mc;
+      L.a.local_base = d_counts;
+      L.a.done_ctr = done + used_done++;
+      L.a.mc_emulate = emulate ? 1u : 0u;
+    }
     batch[fb][strat].clear();
     words[fb][strat] = 0;
     return launch_checked(L, st, fb ? "search kernel (guarded fallback)" : "search kernel (batch)");
   };
   auto add = [&](int fb, const Planned& q) -> sm_status {
     const int k = q.pl.strategy;
-    if (batch[fb][k].size() == (size_t)kMaxBatch || words[fb][k] + q.m > (size_t)kBatchTableWords) {
+    if (batch[fb][k].size() == (size_t)kMaxBatch || words[fb][k] + table_words(q) > (size_t)kBatchTableWords) {
       sm_status s = flush(fb, k);
       if (s != SM_OK) return s;
     }
     batch[fb][k].push_back(&q);
-    words[fb][k] += q.m;
+    words[fb][k] += table_words(q);
     return SM_OK;
   };
+  size_t order_at = 0;
   for (size_t i = 0; i < P; ++i) {
+    const uint32_t* order = orders ? orders + order_at : nullptr;
+    const uint32_t peel = peels ? peels[i] : 0u;
+    order_at += ms[i];
     if (n < ms[i] || lim == 0) continue;  // count stays 0
     Planned& q = plans[i];
     q = Planned{Plan(), ps[i], ms[i], d_counts + i};
-    sm_status s = make_plan(ps[i], ms[i], n, h, P == 1 ? order : nullptr, P == 1 ? peel : 0, strategy, q.pl,
-                            &tinfo, allow_packed);
+    sm_status s = make_plan(ps[i], ms[i], n, h, order, peel, strategy, q.pl, &tinfo, allow_packed);
     if (s != SM_OK) return s;
     use_codes(codes, cb, q.pl);
     if (guard && is_prepacked(q.pl.strategy)) {  // its byte-compare twin, run only if the check fails
       Planned& f = fallback[i];
       f = Planned{Plan(), ps[i], ms[i], d_counts + i};
-      s = make_plan(ps[i], ms[i], n, h, P == 1 ? order : nullptr, P == 1 ? peel : 0, strategy, f.pl, &tinfo,
-                    false);
+      s = make_plan(ps[i], ms[i], n, h, order, peel, strategy, f.pl, &tinfo, false);
       if (s == SM_OK) s = add(1, f);
       if (s != SM_OK) return s;
     }
@@ -750,7 +796,7 @@ sm_status enqueue_count(const uint8_t* p, size_t m, const uint8_t* t, size_t n, 
                         const uint32_t* order, uint32_t peel, int strategy, uint64_t* d_count, cudaStream_t st) {
   const uint8_t* ps[1] = {p};
   const size_t ms[1] = {m};
-  return enqueue_count_batch(ps, ms, 1, t, n, UINT64_MAX, hist, strategy, d_count, st, order, peel);
+  return enqueue_count_batch(ps, ms, 1, t, n, UINT64_MAX, hist, strategy, d_count, st, order, &peel);
 }
 
 // Staging pool of the reporting pass (bytes).  Records: at most 16 B per reported
@@ -841,9 +887,9 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
     };
     for (const Planned& q : plans) {
       if (q.pl.strategy != strat) continue;
-      if (run.size() == (size_t)kMaxBatch || words + q.m > (size_t)kBatchTableWords) flush();
+      if (run.size() == (size_t)kMaxBatch || words + table_words(q) > (size_t)kBatchTableWords) flush();
       run.push_back(&q);
-      words += q.m;
+      words += table_words(q);
     }
     flush();
   }
@@ -1073,6 +1119,31 @@ sm_status sm_count_batch(const uint8_t* const* p, const size_t* m, size_t P, con
   return enqueue_count_batch(p, m, P, t, n, (uint64_t)max_alignments, hist, strategy, d_counts, as_stream(stream));
 }
 
+sm_status sm_count_batch_ordered(const uint8_t* const* p, const size_t* m, size_t P, const uint8_t* t, size_t n,
+                                 size_t max_alignments, const uint64_t* hist, const uint32_t* orders,
+                                 const uint32_t* peels, int strategy, uint64_t* d_counts, void* stream) {
+  if (P == 0) return SM_OK;
+  if (!p || !m || !d_counts) return fail(SM_EINVAL, "NULL argument");
+  if (strategy < SM_STRATEGY_AUTO || strategy > SM_STRATEGY_PAIR) return fail(SM_EINVAL, "bad strategy");
+  size_t at = 0;
+  for (size_t i = 0; i < P; ++i) {
+    if (m[i] == 0) return fail(SM_EINVAL, "m[i] == 0: empty pattern is undefined (reading R2)");
+    if (m[i] > SM_MAX_PATTERN) return fail(SM_EINVAL, "m[i] > SM_MAX_PATTERN (4096)");
+    if (!p[i]) return fail(SM_EINVAL, "p[i] is NULL");
+    if (orders && !valid_permutation(orders + at, m[i])) return fail(SM_EINVAL, "orders[i] is not a permutation");
+    at += m[i];
+  }
+  if (n > 0) {
+    if (!t) return fail(SM_EINVAL, "t is NULL with n > 0");
+    sm_status s = check_device_ptr(t, "t");
+    if (s != SM_OK) return s;
+  }
+  sm_status s = check_device_ptr(d_counts, "d_counts");
+  if (s != SM_OK) return s;
+  return enqueue_count_batch(p, m, P, t, n, (uint64_t)max_alignments, hist, strategy, d_counts, as_stream(stream),
+                             orders, peels);
+}
+
 sm_status sm_count_batch_multicast(const uint8_t* const* p, const size_t* m, size_t P, const uint8_t* t, size_t n,
                                    size_t max_alignments, const uint64_t* hist, int strategy, uint64_t* mc_counts,
                                    void* stream) {
@@ -1091,15 +1162,22 @@ sm_status sm_count_batch_multicast(const uint8_t* const* p, const size_t* m, siz
   }
   if (reinterpret_cast<uintptr_t>(mc_counts) & 7u) return fail(SM_EINVAL, "mc_counts must be 8-byte aligned");
   cudaStream_t st = as_stream(stream);
-  uint64_t* local = nullptr;  // this rank's counts, then one multimem.red per pattern
-  SM_CUDA_TRY(pool_alloc(reinterpret_cast<void**>(&local), P * sizeof(uint64_t), st), "pool_alloc(counts)");
-  sm_status s = enqueue_count_batch(p, m, P, t, n, (uint64_t)max_alignments, hist, strategy, local, st);
-  if (s == SM_OK) {
-    cudaError_t e = launch_nvls_add(local, mc_counts, P, st);
-    if (e == cudaSuccess) ++g_launches;
-    else s = cuda_fail(e, "nvls reduction");
-  }
-  cudaFreeAsync(local, st);
+  // this rank's counts (scratch) + one zeroed done-counter per launch (a call makes at
+  // most 2 (P + 8) launches); the last CTA of each launch adds its patterns' counts to
+  // mc_counts with multimem.red (search_impl.cuh nvls_epilogue)
+  const size_t nd = 2 * (P + 8);
+  uint8_t* scratch = nullptr;
+  SM_CUDA_TRY(pool_alloc(reinterpret_cast<void**>(&scratch), P * sizeof(uint64_t) + nd * 4, st),
+              "pool_alloc(counts)");
+  uint64_t* local = reinterpret_cast<uint64_t*>(scratch);
+  unsigned int* done = reinterpret_cast<unsigned int*>(scratch + P * sizeof(uint64_t));
+  sm_status s = SM_OK;
+  cudaError_t e = cudaMemsetAsync(done, 0, nd * 4, st);
+  if (e != cudaSuccess) s = cuda_fail(e, "cudaMemsetAsync(done counters)");
+  if (s == SM_OK)
+    s = enqueue_count_batch(p, m, P, t, n, (uint64_t)max_alignments, hist, strategy, local, st, nullptr, 0,
+                            mc_counts, done);
+  cudaFreeAsync(scratch, st);
   return s;
 }
 

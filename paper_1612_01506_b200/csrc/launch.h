@@ -40,14 +40,11 @@ cudaError_t launch_stage_expand(const uint8_t* stage, const unsigned long long* 
 cudaError_t launch_pack_text(const uint8_t* base, uint64_t delta, uint64_t n, uint32_t shift, int b, uint8_t* codes,
                              uint64_t code_bytes, uint32_t syms, uint32_t* bad, int num_sms, cudaStream_t st);
 
-// NEXT-4: mc[i] += local[i] through an NVLink multicast address (multimem.red)
-cudaError_t launch_nvls_add(const uint64_t* local, uint64_t* mc, uint64_t P, cudaStream_t st);
-
-// exclusive prefix over items of the sum of wc[item][0..8) (u16 warp counts)
+// exclusive prefix over items of the sum of wc[item][0..8) (u16 warp counts); temp == nullptr:
+// *temp_bytes = the scratch it needs (single-pass decoupled look-back, scan.cu; 2 launches:
+// a memset of the tile status words and the scan)
 cudaError_t exclusive_scan_wc(const uint16_t* wc, uint64_t* out, uint64_t items, void* temp, size_t* temp_bytes,
                               cudaStream_t st);
 
-cudaError_t exclusive_scan_u64(const uint64_t* in, uint64_t* out, uint64_t count, void* temp, size_t* temp_bytes,
-                               cudaStream_t st);
 
 }  // namespace smgpu

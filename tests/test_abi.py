@@ -51,10 +51,12 @@ def test_plan_policy(sm):
     for c in b"ACGT":
         h[c] = 1000
     s, r = sm.sm_plan(b"ACGTACGTACGT", h)
-    assert s == 4 and r == 5                             # DNA: PACKED (2-bit codes); alpha_eff = 512, 512*(1/4)^5 = 1/2
+    # DNA: PACKED (2-bit codes); peel until alpha_eff x prod f <= 32 survivors per warp-block,
+    # which are then verified per lane: alpha_eff = 512, 512 * (1/4)^2 = 32
+    assert s == 4 and r == 2
     h2 = np.ones(256, dtype=np.uint64)
     s, r = sm.sm_plan(b"hello world", h2)
-    assert s == sm.SM_STRATEGY_FILTER and r == 1
+    assert s == sm.SM_STRATEGY_FILTER and r == 2        # phase B peels pi(1) and pi(2)
     s, r = sm.sm_plan(b"ab", h2, strategy=sm.SM_STRATEGY_BLOCK, peel=7)
     assert s == sm.SM_STRATEGY_BLOCK and r == 2           # r <- min(r, m)  (reading R9)
     hz = np.zeros(256, dtype=np.uint64)

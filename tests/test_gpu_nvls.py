@@ -1,4 +1,4 @@
-"""NEXT-4: counting with the all-reduce fused into the kernel epilogue (multimem.red on an
+"""NEXT-4: counting with the all-reduce fused into the search kernel's last-CTA epilogue (multimem.red on an
 NVLink multicast address).  On this single-GPU box the multicast group has one member, so
 the reduction must reproduce the plain counts exactly; with N ranks bound to the same
 multicast object every rank's copy receives the sum (smgpu.h sm_count_batch_multicast)."""
@@ -40,3 +40,19 @@ def test_multicast_counts_equal_plain_counts():
     # oracle parity on a few of them
     for i in range(0, len(pats), 13):
         assert int(want[i]) == oracle.naive_count(pats[i], a[: spec.n // 2 + len(pats[i]) - 1])
+
+
+def test_last_cta_epilogue_protocol_emulated():
+    """The fused epilogue's last-CTA-done protocol, validated on this single-GPU box with
+    SMGPU_NVLS_EMULATE=1 (atomicAdd in place of multimem.red on a unicast buffer): every
+    pattern's count lands exactly once per call, on multi-launch batches, shard limits
+    and guarded PACKED launches (tests/nvls_emulate_workload.py)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SMGPU_NVLS_EMULATE="1")
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "nvls_emulate_workload.py")], env=env,
+                       capture_output=True, text=True, timeout=600)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0 and "mismatches: 0" in out, out[-3000:]

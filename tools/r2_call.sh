@@ -5,6 +5,7 @@ set -x
 OUT=gpurun_out/${TAG:-call}
 mkdir -p $OUT
 S=${SECTIONS:-tests probe alu cfg c5 ncu san}
+# also: ab (tools/r2_ab.sh), abl (tools/ablation_r2.py orders + r sweep), bench (default bench line)
 has() { case " $S " in *" $1 "*) return 0;; esac; return 1; }
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > $OUT/smi.txt 2>&1
 if has tests; then
@@ -33,6 +34,16 @@ if has ncu; then
 fi
 if has san; then
   OUT=$OUT/san bash tools/sanitize.sh > $OUT/sanitize.log 2>&1
+fi
+if has ab; then
+  TAG=${TAG:-call} bash tools/r2_ab.sh > $OUT/ab.log 2>&1
+fi
+if has abl; then
+  timeout 900 python tools/ablation_r2.py --mode orders --configs c2,c3,c1 > $OUT/ablation_orders.jsonl 2> $OUT/ablation_orders.err
+  timeout 900 python tools/ablation_r2.py --mode rsweep --configs c1,c3,c4 --lengths 8,16,32,128 > $OUT/ablation_rsweep.jsonl 2> $OUT/ablation_rsweep.err
+fi
+if has bench; then
+  timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err
 fi
 if [ -n "$EXTRA" ]; then bash -c "$EXTRA"; fi
 echo done
