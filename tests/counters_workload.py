@@ -19,56 +19,6 @@ torch.cuda.set_device(0)
 assert "counters" in sm.sm_version(), sm.sm_version()
 rng = np.random.default_rng(77)
 fails = 0
-# PACKED's per-lane survivor verification (search_impl.cuh verify_code_survivors) is not
-# Alg. 4's loop: with it on, PACKED is pinned to the hybrid model below; the exact Alg. 4
-# pin of PACKED runs in a second process with SMGPU_PACKED_SPARSE=0 (test_gpu_counters.py)
-SPARSE = int(os.environ.get("SMGPU_PACKED_SPARSE", "128"))
-
-
-def packed_hybrid_model(p, a, alpha, pi, r, b, sparse_max):
-    """Expected counters of a PACKED pass: blocks of alpha alignments from 0; after r peeled
-    steps a block with <= sparse_max survivors verifies them one by one against the
-    pattern's natural-order code words (32 / b positions per word, first mismatch ends it),
-    else it runs Alg. 4's ordered loop (a step while any alignment of the block survives)."""
-    m, n = len(p), a.size
-    A = n - m + 1
-    pv = np.frombuffer(p, dtype=np.uint8)
-    nb = -(-A // alpha)
-    surv = np.ones(A, dtype=bool)
-    for k in range(min(r, m)):
-        surv &= a[pi[k]:pi[k] + A] == pv[pi[k]]
-    pad = np.zeros(nb * alpha, dtype=bool)
-    pad[:A] = surv
-    blk = pad.reshape(nb, alpha)
-    cnt = blk.sum(axis=1)
-    steps = np.full(nb, min(r, m), dtype=np.int64)
-    res = {"blocks": nb, "sparse_blocks": 0, "code_survivors": 0, "code_words": 0}
-    if r >= m:
-        res["steps"] = int(steps.sum())
-        return res
-    sparse = cnt <= sparse_max if sparse_max else np.zeros(nb, dtype=bool)
-    res["sparse_blocks"] = int(sparse.sum())
-    cur = blk.copy()
-    for k in range(r, m):  # dense blocks: Alg. 4's loop
-        alive = cur.any(axis=1) & ~sparse
-        steps += alive
-        col = np.zeros(nb * alpha, dtype=bool)
-        col[:A] = a[pi[k]:pi[k] + A] == pv[pi[k]]
-        cur &= col.reshape(nb, alpha)
-    res["steps"] = int(steps.sum())
-    per_word = 32 // b
-    nw = -(-m // per_word)
-    idx = np.flatnonzero((blk & sparse[:, None]).ravel())
-    res["code_survivors"] = int(idx.size)
-    for x in idx:
-        eq = a[x:x + m] == pv
-        words = nw
-        for w in range(nw):
-            if not eq[w * per_word:(w + 1) * per_word].all():
-                words = w + 1
-                break
-        res["code_words"] += words
-    return res
 
 
 def run(p, a, t, strategy, order=None, peel=0):
@@ -97,21 +47,13 @@ for n in ((1 << 20) + 333, (16 << 20) + 77):
                 for peel in (1, 2, 5):
                     got, c = run(p, a, t, strategy, order=pi.tolist(), peel=peel)
                     want = oracle.naive_count(p, a)
-                    if strategy == sm.SM_STRATEGY_PACKED and SPARSE:
-                        b = 1 if syms.size <= 2 else 2
-                        hm = packed_hybrid_model(p, a, c["alpha_eff"], pi, peel, b, SPARSE)
-                        ok = got == want and all(c[k] == v for k, v in hm.items())
-                        fails += not ok
-                        print(("ok " if ok else "MISMATCH ") + f"PACKED-sparse n={n} sigma={syms.size} m={m} r={peel} "
-                              f"alpha={c['alpha_eff']} got={ {k: c[k] for k in hm} } model={hm} count={got}/{want}")
-                        continue
                     steps, blocks = oracle.alg4_steps(p, a, alpha=c["alpha_eff"], pi=pi, r=peel)
                     ok = got == want and c["steps"] == steps and c["blocks"] == blocks
                     fails += not ok
                     print(("ok " if ok else "MISMATCH ") + f"n={n} sigma={syms.size} m={m} strat={strategy} r={peel} "
                           f"alpha={c['alpha_eff']} steps={c['steps']}/{steps} blocks={c['blocks']}/{blocks} "
                           f"count={got}/{want}")
-            if syms.size <= 4 and not SPARSE:  # batches of >= 2 patterns: PACKED on the text's code array (NEXT-3)
+            if syms.size <= 4:  # batches of >= 2 patterns run PACKED on the text's code array (NEXT-3)
                 sm.sm_counters(reset=True)
                 d2 = torch.zeros(2, dtype=torch.int64, device="cuda")
                 sm.sm_count_batch([p, p], t, d2, hist=oracle.hist(a), strategy=sm.SM_STRATEGY_PACKED)
@@ -131,8 +73,6 @@ for n in ((1 << 20) + 333, (16 << 20) + 77):
                 A = n - m + 1
                 a1, a2 = int(pi[0]), int(pi[1])
                 surv = int(np.count_nonzero((a[a1:a1 + A] == p[a1]) & (a[a2:a2 + A] == p[a2])))
-                if m in (3, 4) and fs == sm.SM_STRATEGY_FILTER:  # one exact pass per queued chunk: survivors = matches
-                    surv = oracle.naive_count(p, a)
                 ok = c["filter_survivors"] == surv and got == oracle.naive_count(p, a)
                 fails += not ok
                 print(("ok " if ok else "MISMATCH ") + f"FILTER/PAIR({fs}) n={n} sigma={syms.size} m={m} "

@@ -10,13 +10,10 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("sparse", ["0", "128"])
-def test_counters_match_oracle_alg4_steps(sparse):
-    """sparse = 0: BLOCK and PACKED both pinned to oracle.alg4_steps exactly; 128 (the default):
-    PACKED's per-lane survivor verification pinned to the hybrid model of the workload."""
+def test_counters_match_oracle_alg4_steps():
     from paper_1612_01506_b200 import _build
     assert os.path.exists(_build.build(counters=True))
-    env = dict(os.environ, SMGPU_LIB="counters", SMGPU_PACKED_SPARSE=sparse)
+    env = dict(os.environ, SMGPU_LIB="counters")
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "counters_workload.py")], env=env,
                        capture_output=True, text=True, timeout=900)
     out = r.stdout + r.stderr
