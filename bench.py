@@ -573,6 +573,28 @@ def run_native(args):
         report = {"value": spec.n * P / (r_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_pass": r_ms,
                   "positions_written": tot, "position_bytes": 8 * tot,
                   "passes": "one text read per pattern (staged match records + expand), see DESIGN.md"}
+        # per pattern length: report pass time vs the same patterns' count launches (diagnostic)
+        rp = {}
+        for m in lens:
+            idx = [i for i, p in enumerate(pats) if p.m == m]
+            sub = sm.PatternBatch([pdata[i] for i in idx])
+            dsub = torch.zeros(len(idx), dtype=torch.int64, device=dev)
+            subtot = int(counts_host[idx].sum())
+
+            def rep_m():
+                sm.sm_report_batch(sub, held, posbuf[: max(subtot, 1)], dsub, hist=hh,
+                                   max_alignments=shard.owned_bytes)
+            rep_m()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rep_m()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms_m = e0.elapsed_time(e1)
+            rp[str(m)] = {"GBps": round(float(local_bytes[idx].sum()) / (ms_m * 1e-3) / 1e9, 1),
+                          "positions": subtot, "report_over_count": round(
+                              ms_m * 1e3 / len(idx) / per_m[str(m)]["us_per_launch"], 3)}
+        report["per_m"] = rp
         del posbuf
         if not args.no_dense:
             report["dense"] = dense_report(sm, synth, dev, stream, peak)

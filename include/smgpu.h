@@ -251,10 +251,7 @@ sm_status sm_plan(const uint8_t* p, size_t m, const uint64_t* hist, const uint32
  *   out[5] FILTER valid alignments matching pi(1) and pi(2)
  *   out[6] FILTER pattern positions compared while verifying those
  *   out[7] BLOCK/PACKED alignments per warp-block (max over launches)
- *   out[8] PACKED warp-blocks finished by per-lane survivor verification
- *   out[9] PACKED survivors of the peeled steps verified per lane there
- *   out[10] PACKED 32-bit code words compared while verifying them
- * (out: host u64[11]) */
+ * (out: host u64[8]) */
 sm_status sm_counters(uint64_t* out, int reset);
 
 /* Thread-local status of the last failing call on this thread (SM_OK if none

@@ -47,7 +47,7 @@ EXPORTED_SYMBOLS = (
     "sm_clear_error", "sm_status_string", "sm_version", "sm_launch_count", "sm_counters",
 )
 COUNTER_NAMES = ("warp_tiles", "blocks", "steps", "filter_chunks", "filter_queued", "filter_survivors",
-                 "filter_verify", "alpha_eff", "sparse_blocks", "code_survivors", "code_words")
+                 "filter_verify", "alpha_eff")
 
 
 class SmError(RuntimeError):

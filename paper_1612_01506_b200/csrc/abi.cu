@@ -167,9 +167,6 @@ struct Tunables {
   uint64_t dispatch_min_bytes = 64ull << 20;  // ... when the call streams at least this much text (n x P)
   uint64_t dispatch_min_bytes_single = 512ull << 20;  // single-pattern calls (the counter's memset
                                                       // costs more than it gains on short launches)
-  uint32_t packed_sparse = 128;  // PACKED: per-lane survivor verification when a warp-block has <= this many
-                                 // survivors after the peeled steps (0: Alg. 4's ordered loop always)
-  double packed_peel_surv = 32;  // PACKED + sparse: AUTO r = smallest with alpha_eff prod f <= this
 };
 
 const Tunables& tunables() {
@@ -194,8 +191,6 @@ const Tunables& tunables() {
     if (const char* e = std::getenv("SMGPU_DISPATCH_MIN_MB")) x.dispatch_min_bytes = (uint64_t)std::atoll(e) << 20;
     if (const char* e = std::getenv("SMGPU_DISPATCH_MIN_MB_SINGLE"))
       x.dispatch_min_bytes_single = (uint64_t)std::atoll(e) << 20;
-    if (const char* e = std::getenv("SMGPU_PACKED_SPARSE")) x.packed_sparse = (uint32_t)std::atoi(e);
-    if (const char* e = std::getenv("SMGPU_PACKED_PEEL_SURV")) x.packed_peel_surv = std::atof(e);
     if (x.ctas_pre < 1 || x.ctas_pre > 4) x.ctas_pre = 3;
     if (const char* e = std::getenv("SMGPU_STAGES_PRE")) x.max_stages_pre = (uint32_t)std::atoi(e);
     if (x.max_stages_pre < 2 || x.max_stages_pre > (uint32_t)kMaxStages) x.max_stages_pre = 6;
@@ -449,12 +444,8 @@ sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist
     // for r ("it is less probable that all the alpha comparisons
     // fail at the same time") at the warp's alpha_eff = 32 lanes x 16 x CPL, capped at 2048.
     double surv = std::min(32.0 * 16.0 * pl.cpl, 2048.0);
-    // PACKED with per-lane survivor verification: peel only until the warp-block's expected
-    // survivors are few enough to verify one by one (search_impl.cuh verify_code_survivors)
-    const double target = is_packed(pl.strategy) && tunables().packed_sparse ? tunables().packed_peel_surv : 0.5;
-    if (is_packed(pl.strategy)) surv = 32.0 * 16.0 * pl.cpl;
     uint32_t r = 0;
-    while (r < m && surv > target) surv *= freq(r++);
+    while (r < m && surv > 0.5) surv *= freq(r++);
     const int rb = (int)r + tunables().peel_bias;  // tuning knob (0 by default)
     peel = rb < 1 ? 1u : (uint32_t)rb;
   }
@@ -550,11 +541,8 @@ struct Planned {
   uint64_t* count_out;
 };
 
-// kernel-parameter table entries of a planned pattern: its m (offset, symbol) pairs in
-// pi order, + its natural-order code words for PACKED
-size_t table_words(const Planned& q) {
-  return q.m + (is_packed(q.pl.strategy) ? packed_code_words((uint32_t)q.m, code_bits(q.pl.strategy)) : 0u);
-}
+// kernel-parameter table entries of a planned pattern: its m (offset, symbol) pairs in pi order
+size_t table_words(const Planned& q) { return q.m; }
 
 // Build one launch over patterns `ps` (same strategy; <= kMaxBatch, table <= kTableLarge).
 // The tile is the plan's (large texts: 32 KiB); the batching loops keep a launch's
@@ -579,17 +567,7 @@ void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_
       const uint32_t v = packed ? ((sym >> L.a.code_shift) & ((1u << cbits) - 1u)) : sym;
       L.e.push_back(q->pl.order[k] | (v << 16));
     }
-    if (packed) {  // the pattern's codes in natural order (per-lane survivor verification)
-      const size_t w0 = L.e.size();
-      L.e.resize(w0 + packed_code_words((uint32_t)q->m, (int)cbits), 0u);
-      for (size_t j = 0; j < q->m; ++j) {
-        const uint32_t v = (q->p[j] >> L.a.code_shift) & ((1u << cbits) - 1u);
-        const size_t bit = j * cbits;
-        L.e[w0 + bit / 32] |= v << (bit % 32);
-      }
-    }
   }
-  L.a.sparse_max = packed ? tunables().packed_sparse : 0u;
   L.a.npat = (uint32_t)ps.size();
   L.a.tbl_words = (uint32_t)L.e.size();
   L.a.ctr = counters_ptr();
@@ -599,7 +577,7 @@ void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_
   L.a.list_off = (kTblOff + 127) & ~127u;
   // reporting: kEpiStage keeps one 32 CPL-mask bitmap per warp (<= 512 B), the overflow
   // pass (kEpiWrite) a kListCap-entry position list per warp
-  const uint32_t list_bytes = epilogue == kEpiCount ? 0u
+  const uint32_t list_bytes = is_count_epi(epilogue) ? 0u
                               : epilogue == kEpiStage ? (uint32_t)(kConsumerWarps * 32 * 8 * 2)
                                                       : (uint32_t)(kConsumerWarps * kListCap * 2);
   L.a.pack_off = (L.a.list_off + list_bytes + 127) & ~127u;
@@ -732,7 +710,7 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
   auto flush = [&](int fb, int strat) -> sm_status {
     if (batch[fb][strat].empty()) return SM_OK;
     HostLaunch L;
-    build_launch(batch[fb][strat], t, n, lim, kEpiCount, L);
+    build_launch(batch[fb][strat], t, n, lim, mc ? kEpiCountMc : kEpiCount, L);
     L.a.codes = codes.p;
     if (guard && (fb || is_prepacked(strat))) {
       L.a.guard = guard;

@@ -33,13 +33,15 @@ enum Strategy : int { kFilter = 1, kBlock = 2, kPacked1 = 3, kPacked2 = 4, kPair
 __host__ __device__ constexpr bool is_packed(int s) { return s == kPacked1 || s == kPacked2 || s >= kPacked1Pre; }
 __host__ __device__ constexpr bool is_prepacked(int s) { return s >= kPacked1Pre; }
 __host__ __device__ constexpr int code_bits(int s) { return (s == kPacked2 || s == kPacked2Pre) ? 2 : 1; }
-__host__ __device__ constexpr uint32_t packed_code_words(uint32_t m, int b) { return (m * (uint32_t)b + 31u) / 32u; }
 // kEpiCount: per-pattern counts.  kEpiStage: reporting pass 1 -- per-(pattern, tile) counts
 // plus the tile's matches staged compactly in global memory (per-warp u16 offset lists
 // or bitmaps), expanded into positions by stage_expand_kernel after the scan: the
 // text is read once.  kEpiWrite: reporting fallback for the tiles whose staging did
 // not fit the pool (overflow queue): recompute from the text, write positions.
-enum Epilogue : int { kEpiCount = 0, kEpiStage = 1, kEpiWrite = 2 };
+// kEpiCountMc: kEpiCount + the NEXT-4 last-CTA epilogue (multimem.red of the launch's
+// counts to an NVLink multicast address, LaunchArgs::mc_base) -- a separate instantiation.
+enum Epilogue : int { kEpiCount = 0, kEpiStage = 1, kEpiWrite = 2, kEpiCountMc = 3 };
+__host__ __device__ constexpr bool is_count_epi(int e) { return e == kEpiCount || e == kEpiCountMc; }
 
 // Staged reporting (kEpiStage): every compare warp with matches in a work item writes
 // one self-describing record into its own chunk of the staging pool (kStageChunk
@@ -123,9 +125,7 @@ struct LaunchArgs {
                              // set the code field was chosen for (a caller histogram that is not t's)
   uint32_t guard_mode;       // 0: always run; kGuardClear: run only if *guard == 0 (PACKED on a caller
                              // histogram); kGuardSet: run only if *guard != 0 (its byte-compare fallback)
-  uint32_t sparse_max;       // PACKED: a warp-block with <= this many survivors after the r peeled steps is
-                             // finished by per-lane verification of its survivors (0: Alg. 4's loop always)
-  // NEXT-4 (count epilogue): non-null = after every CTA's atomics, the last CTA to finish
+  // NEXT-4 (kEpiCountMc): after every CTA's atomics, the last CTA to finish
   // (done_ctr, zeroed by the host) adds each pattern's count, read from count_out, to
   // mc_base + (count_out - local_base) with one multimem.red (NVLink multicast: the
   // switch adds it to every rank's copy).  mc_emulate: plain atomicAdd instead (tests on
@@ -147,16 +147,12 @@ enum Counter : int {
   kCtrSurvivors = 5,     // FILTER: valid alignments matching pi(1) and pi(2) (entering verification)
   kCtrVerify = 6,        // FILTER: pattern positions compared while verifying survivors
   kCtrAlphaEff = 7,      // BLOCK / PACKED: alignments per warp-block (max)
-  kCtrSparseBlocks = 8,  // PACKED: warp-blocks finished by per-lane survivor verification (of kCtrBlocks)
-  kCtrCodeSurvivors = 9, // PACKED: survivors of the r peeled steps verified per lane in those blocks
-  kCtrCodeWords = 10,    // PACKED: 32-bit code words compared while verifying them
-  kCounters = 11
+  kCounters = 8
 };
 
 // Kernel parameters: everything per launch, no __constant__ state, so launches on
 // different streams never race.  Table entry = off(pi(k)) | p[pi(k)] << 16
-// (PACKED: the symbol's b-bit code instead of the byte; followed by the pattern's codes
-// in natural order as packed_code_words(m, b) words: code(p[j]) at bits b j of the string).
+// (PACKED: the symbol's b-bit code instead of the byte).
 template <int CAP>
 struct LaunchParams {
   LaunchArgs a;

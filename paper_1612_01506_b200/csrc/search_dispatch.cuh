@@ -66,9 +66,21 @@ cudaError_t launch_c(const HostLaunch& L, cudaStream_t st) {
   }
 }
 
+// NEXT-4 count launches with the multicast epilogue: large tables only (fewer instantiations)
+template <int STRAT>
+cudaError_t launch_mc(const HostLaunch& L, cudaStream_t st) {
+  switch (L.cpl) {
+    case 8: return launch_one<STRAT, kEpiCountMc, kTableLarge, 8>(L, st);
+    case 4: return launch_one<STRAT, kEpiCountMc, kTableLarge, 4>(L, st);
+    case 2: return launch_one<STRAT, kEpiCountMc, kTableLarge, 2>(L, st);
+    default: return launch_one<STRAT, kEpiCountMc, kTableLarge, 1>(L, st);
+  }
+}
+
 template <int STRAT>
 cudaError_t launch_strategy(const HostLaunch& L, cudaStream_t st) {
   if (L.epilogue == kEpiCount) return launch_c<STRAT, kEpiCount>(L, st);
+  if (L.epilogue == kEpiCountMc) return launch_mc<STRAT>(L, st);
   if (L.epilogue == kEpiStage) return launch_c<STRAT, kEpiStage>(L, st);
   return launch_c<STRAT, kEpiWrite>(L, st);
 }

@@ -126,7 +126,7 @@ struct Ctr {
   __device__ __forceinline__ void flush(unsigned long long* out, int lane) {
     if (!out) return;
     for (int i = 0; i < kCounters; ++i) {
-      const bool uniform = i != kCtrSurvivors && i != kCtrVerify && i != kCtrCodeSurvivors && i != kCtrCodeWords;
+      const bool uniform = i != kCtrSurvivors && i != kCtrVerify;
       if (i == kCtrAlphaEff) {
         if (lane == 0 && v[i]) atomicMax(out + i, v[i]);
       } else if (v[i] && (!uniform || lane == 0)) {
@@ -396,75 +396,6 @@ __device__ __forceinline__ uint32_t verify_survivors(const Pat& pt, const uint8_
   return g;
 }
 
-// FILTER phase B for patterns of m = 3 or 4 (all of p inside 4 consecutive bytes):
-// one exact pass over the queued chunk instead of pi(1), pi(2) and a per-survivor loop --
-// the m compares of Alg. 1 for 16 alignments at once, y = OR_j (window_j ^ p[j]) per word,
-// an alignment matches iff its byte of y is zero (PAPER.md:94's found, every position
-// compared: no early exit is needed for so short a pattern).  O0 = pre - a1 = byte offset
-// of alignment u = 16c relative to 16c (a1 <= 3: 0, 13, 14 or 15; warp-uniform, compile
-// time), so every window is a compile-time funnel shift of the chunk's words.
-template <int O0>
-__device__ __forceinline__ uint32_t short_entry(const Pat& pt, const uint8_t* buf, uint32_t c, bool edge, int32_t rlo,
-                                                int32_t rhi, const uint32_t (&bc)[4]) {
-  static_assert(O0 == 0 || (O0 >= 13 && O0 <= 15), "m <= 4 puts pi(1) at offset 0..3");
-  const uint8_t* base = buf + 16u * c;
-  uint32_t w[12];
-  {
-    SMGPU_DCHECK(16u * c + (O0 ? 48u : 32u) <= pt.lim);
-    const uint4 b0 = lds128(base), b1 = lds128(base + 16);
-    w[0] = b0.x; w[1] = b0.y; w[2] = b0.z; w[3] = b0.w;
-    w[4] = b1.x; w[5] = b1.y; w[6] = b1.z; w[7] = b1.w;
-    if (O0) {
-      const uint4 b2 = lds128(base + 32);
-      w[8] = b2.x; w[9] = b2.y; w[10] = b2.z; w[11] = b2.w;
-    } else {
-      w[8] = w[9] = w[10] = w[11] = 0u;
-    }
-  }
-  uint32_t y[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    if (j == 3 && pt.m == 3) break;  // warp-uniform
-    const int o = O0 + j, q = o >> 2, sh = 8 * (o & 3);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t win = sh ? __funnelshift_r(w[q + i], w[q + i + 1], sh) : w[q + i];
-      y[i] |= win ^ bc[j];
-    }
-  }
-  Found4 F = edge ? found_from_mask16(range_mask16_rel((int32_t)(16u * c), rlo, rhi)) : found_all();
-  F.f0 &= eq_flags_raw(y[0], 0u);
-  F.f1 &= eq_flags_raw(y[1], 0u);
-  F.f2 &= eq_flags_raw(y[2], 0u);
-  F.f3 &= eq_flags_raw(y[3], 0u);
-  return compress_found(F);
-}
-
-template <int O0, class Sink>
-__device__ __forceinline__ void short_drain(const Pat& pt, const uint8_t* buf, int lane, const uint16_t* qc,
-                                            uint32_t qlen, bool edge, int32_t rlo, int32_t rhi, Sink& sink, Ctr& C) {
-  uint32_t bc[4] = {0u, 0u, 0u, 0u};  // p[j] broadcast, natural order (from the pi-ordered table)
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    if (k < (int)pt.m) {
-      const uint32_t e = pt.tbl[k];
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if ((e & 0xFFFFu) == (uint32_t)j) bc[j] = (e >> 16) * 0x01010101u;
-    }
-  }
-  for (uint32_t b0 = 0; b0 < qlen; b0 += 32) {
-    const uint32_t i = b0 + lane;
-    uint32_t c = 0, g = 0;
-    if (i < qlen) {
-      c = qc[i];
-      g = short_entry<O0>(pt, buf, c, edge, rlo, rhi, bc);
-      C.add(kCtrSurvivors, __popc(g));
-    }
-    sink(c, g, lane);
-  }
-}
-
 // IN_G: input is a compressed found word (FILTER/BLOCK), else a 16-bit mask.
 template <bool IN_G = true>
 struct WriteSink {
@@ -586,25 +517,11 @@ __device__ __forceinline__ void filter_tile_q(const Pat& pt, const uint8_t* buf,
     }
     C.add(kCtrQueued, qlen);
     __syncwarp();
-    bool short_done = false;
-    if constexpr (!PA) {  // FILTER, m = 3 or 4 (warp-uniform): one exact pass per queued chunk
-      if (pt.m == 3 || pt.m == 4) {
-        switch (pt.pre - pt.a1) {
-          case 0: short_drain<0>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink, C); break;
-          case 13: short_drain<13>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink, C); break;
-          case 14: short_drain<14>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink, C); break;
-          default: short_drain<15>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink, C); break;
-        }
-        short_done = true;
-      }
-    }
-    if (!short_done) {
-      switch ((pt.s2 >> 2) & 3u) {  // warp-uniform
-        case 0: filter_drain<0>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink, C); break;
-        case 1: filter_drain<1>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink, C); break;
-        case 2: filter_drain<2>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink, C); break;
-        default: filter_drain<3>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink, C); break;
-      }
+    switch ((pt.s2 >> 2) & 3u) {  // warp-uniform
+      case 0: filter_drain<0>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink, C); break;
+      case 1: filter_drain<1>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink, C); break;
+      case 2: filter_drain<2>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink, C); break;
+      default: filter_drain<3>(pt, buf, lane, qc, qlen, edge, rlo, rhi, sink, C); break;
     }
     __syncwarp();
   }
@@ -784,42 +701,6 @@ __device__ __forceinline__ void packed_step(uint32_t (&F)[CPL], const uint32_t (
   }
 }
 
-// Sparse finish of a PACKED warp-block: after the r peeled steps (which run over all of
-// the warp's 512 CPL alignments), a warp with few survivors left verifies them per lane
-// instead of running more warp-wide steps -- Alg. 3's inner loop per surviving alignment
-// (first mismatch ends it), on b-bit codes in the pattern's natural
-// order, 32 code bits = 32 / b pattern positions per compare.  (Alg. 4's loop keeps a
-// warp-block alive while ANY of its alignments survives: ~log2(alpha_eff) steps on
-// binary text at alpha_eff = 4096.)  f: flag word, bit j (b = 1) or bit 2j (b = 2) <->
-// tile-relative alignment xbase + j; pw: the pattern's code words.  Any order of the
-// compares gives Alg. 1's answer, so the result is unchanged.
-template <int B>
-__device__ __forceinline__ uint32_t verify_code_survivors(uint32_t f, uint32_t xbase, const uint32_t* pk32,
-                                                          uint32_t pk_words, const uint32_t* pw, uint32_t m,
-                                                          Ctr& C) {
-  const uint32_t nw = packed_code_words(m, B);
-  const uint32_t tail = (m * B) & 31u;
-  const uint32_t last_mask = tail ? (1u << tail) - 1u : 0xFFFFFFFFu;
-  uint32_t todo = f;
-  while (todo) {
-    const uint32_t bit = __ffs(todo) - 1;
-    todo &= todo - 1;
-    C.add(kCtrCodeSurvivors, 1);
-    uint32_t pos = B * (xbase + (B == 2 ? bit >> 1 : bit));  // code-bit offset of the alignment
-    for (uint32_t k = 0; k < nw; ++k, pos += 32u) {
-      SMGPU_DCHECK((pos >> 5) + 1u < pk_words);
-      const uint32_t w = __funnelshift_r(pk32[pos >> 5], pk32[(pos >> 5) + 1], pos & 31u);
-      const uint32_t diff = (w ^ pw[k]) & (k + 1 == nw ? last_mask : 0xFFFFFFFFu);
-      C.add(kCtrCodeWords, 1);
-      if (diff) {
-        f &= ~(1u << bit);
-        break;
-      }
-    }
-  }
-  return f;
-}
-
 // One warp's share of a PACKED tile: pack this lane's chunks (and a share of the
 // halo), then -- after the CTA's consumer warps have packed the whole tile --
 // Alg. 4 on the codes: r peeled steps, then the pi-ordered loop with a warp-uniform
@@ -833,7 +714,7 @@ __device__ __forceinline__ int packed_tile(const Pat& pt, const uint8_t* buf, ui
                                            uint32_t nchunks,
                                             uint32_t code_shift, uint32_t cw0, int warp, int lane, bool edge,
                                             int32_t rlo, int32_t rhi, uint64_t* empty_bar, uint32_t* m_out,
-                                            uint32_t* base_out, uint32_t sparse_max, Ctr& C) {
+                                            uint32_t* base_out, Ctr& C) {
   const bool valid_block = !edge || (rlo < (int32_t)(16u * cw0 + 512u * CPL) && rhi > (int32_t)(16u * cw0));
   if constexpr (PRE) {
     pk = const_cast<uint8_t*>(buf);
@@ -891,30 +772,16 @@ __device__ __forceinline__ int packed_tile(const Pat& pt, const uint8_t* buf, ui
     uint32_t k = 0;
     for (; k < pt.r1; ++k) step_reg(pt.tbl[k]);
     for (; k < pt.r; ++k) step_mem(pt.tbl[k]);
-    bool sparse = false;
-    if (sparse_max && k < pt.m) {  // few survivors: per-lane verification (warp-uniform decision)
-      uint32_t pc = 0;
+    for (; k < pt.m; ++k) {                // ordered loop with exit test
+      uint32_t any = 0;
 #pragma unroll
-      for (int it = 0; it < D; ++it) pc += __popc(F[it]);
-      sparse = __reduce_add_sync(0xFFFFFFFFu, pc) <= sparse_max;
-    }
-    if (sparse) {
-#pragma unroll
-      for (int it = 0; it < D; ++it)
-        F[it] = verify_code_survivors<1>(F[it], 32u * (dc0 + it * 32u), pk32, pk_words, pt.tbl + pt.m, pt.m, C);
-    } else {
-      for (; k < pt.m; ++k) {                // ordered loop with exit test
-        uint32_t any = 0;
-#pragma unroll
-        for (int it = 0; it < D; ++it) any |= F[it];
-        if (!__any_sync(0xFFFFFFFFu, any != 0)) break;
-        step(pt.tbl[k]);
-      }
+      for (int it = 0; it < D; ++it) any |= F[it];
+      if (!__any_sync(0xFFFFFFFFu, any != 0)) break;
+      step(pt.tbl[k]);
     }
     if (valid_block) {
       C.add(kCtrBlocks, 1);
       C.add(kCtrSteps, k);
-      if (sparse) C.add(kCtrSparseBlocks, 1);
     }
 #pragma unroll
     for (int it = 0; it < D; ++it) {
@@ -937,30 +804,16 @@ __device__ __forceinline__ int packed_tile(const Pat& pt, const uint8_t* buf, ui
   uint32_t k = 0;  // peeled: register-window steps first (see above)
   for (; k < pt.r1; ++k) packed_step<CPL, B, 1>(F, W0, W1, pk32, qbase, lane, pt.tbl[k], pk_words);
   for (; k < pt.r; ++k) packed_step<CPL, B, 2>(F, W0, W1, pk32, qbase, lane, pt.tbl[k], pk_words);
-  bool sparse = false;
-  if (sparse_max && k < pt.m) {  // few survivors: per-lane verification (warp-uniform decision)
-    uint32_t pc = 0;
+  for (; k < pt.m; ++k) {  // ordered loop with exit test, warp-uniform
+    uint32_t any = 0;
 #pragma unroll
-    for (int it = 0; it < CPL; ++it) pc += __popc(F[it]);
-    sparse = __reduce_add_sync(0xFFFFFFFFu, pc) <= sparse_max;
-  }
-  if (sparse) {
-#pragma unroll
-    for (int it = 0; it < CPL; ++it)
-      F[it] = verify_code_survivors<B>(F[it], 16u * (cw0 + it * 32u + lane), pk32, pk_words, pt.tbl + pt.m, pt.m, C);
-  } else {
-    for (; k < pt.m; ++k) {  // ordered loop with exit test, warp-uniform
-      uint32_t any = 0;
-#pragma unroll
-      for (int it = 0; it < CPL; ++it) any |= F[it];
-      if (!__any_sync(0xFFFFFFFFu, any != 0)) break;
-      packed_step<CPL, B>(F, W0, W1, pk32, qbase, lane, pt.tbl[k], pk_words);
-    }
+    for (int it = 0; it < CPL; ++it) any |= F[it];
+    if (!__any_sync(0xFFFFFFFFu, any != 0)) break;
+    packed_step<CPL, B>(F, W0, W1, pk32, qbase, lane, pt.tbl[k], pk_words);
   }
   if (valid_block) {
     C.add(kCtrBlocks, 1);
     C.add(kCtrSteps, k);
-    if (sparse) C.add(kCtrSparseBlocks, 1);
   }
 #pragma unroll
   for (int it = 0; it < CPL; ++it) {
@@ -1154,14 +1007,16 @@ __device__ __forceinline__ void stage_warp(const LaunchArgs& a, uint16_t* bm, St
 
 }  // namespace
 
-// NEXT-4 epilogue (count launches with a.mc_base): the last CTA to finish reads the
+// NEXT-4 epilogue (kEpiCountMc launches): the last CTA to finish reads the
 // launch's per-pattern counts (complete: every CTA's atomics happened before its
 // done_ctr increment, fenced) and one warp adds each to the NVLink multicast address
 // with multimem.red -- the all-reduce of PAPER.md:36's counting version across ranks,
-// done by the switch, no collective call and no extra launch.  Out of line and after
-// the work loop, so the convergent asm does not touch the hot loop.
+// done by the switch, no collective call and no extra launch.  Only the kEpiCountMc
+// instantiations contain it: inline asm is convergent, and its presence anywhere in a
+// kernel made the compiler wrap the kernel's divergent regions in reconvergence
+// barriers (PAIR count kernel: 84 -> 213 BSSY, about -4 % on every count launch).
 template <int CAP>
-__device__ __noinline__ void nvls_epilogue(const LaunchParams<CAP>& P, int warp, int lane, uint32_t* s_flag) {
+__device__ __forceinline__ void nvls_epilogue(const LaunchParams<CAP>& P, int warp, int lane, uint32_t* s_flag) {
   const LaunchArgs& a = P.a;
   named_bar_sync(1, kConsumerWarps * 32);  // this CTA's compare warps have all added their counts
   if (warp == 0 && lane == 0) {
@@ -1287,7 +1142,7 @@ __global__ void __launch_bounds__(kThreads,
         if constexpr (STRAT == kPair) pair_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, sink, cc);
         else filter_tile<CPL>(pt, buf, cw0, lane, qc, edge, rlo, rhi, sink, cc);
       };
-      if (EPI == kEpiCount) {
+      if (is_count_epi(EPI)) {
         CountSink cs;
         ftile(cs, C);
         acc += cs.n;
@@ -1322,14 +1177,14 @@ __global__ void __launch_bounds__(kThreads,
       uint8_t* pk = smem + a.pack_off + par_pk * a.pack_bytes;
       const int units = packed_tile<CPL, B, PRE>(pt, buf, pk, PRE ? d.stage_len / 4u : a.pack_bytes / 4u,
                                                  d.stage_len / 16u, a.code_shift, cw0, warp, lane, edge, rlo, rhi,
-                                                 &empty[s], mk, mbase, a.sparse_max, C);
+                                                 &empty[s], mk, mbase, C);
       released = !PRE;  // packed_tile released the stage after packing (PRE: it was read until now)
       par_pk ^= 1u;
       uint32_t tc = 0;
 #pragma unroll
       for (int it = 0; it < CPL; ++it)
         if (it < units) tc += __popc(mk[it]);
-      if (EPI == kEpiCount) {
+      if (is_count_epi(EPI)) {
         acc += tc;
       } else if (EPI == kEpiStage) {
         constexpr bool kWide = B == 1 && CPL >= 2;  // 32-bit masks of 32 alignments
@@ -1356,7 +1211,7 @@ __global__ void __launch_bounds__(kThreads,
       uint32_t tc = 0;
 #pragma unroll
       for (int it = 0; it < CPL; ++it) tc += __popc(g[it]);
-      if (EPI == kEpiCount) {
+      if (is_count_epi(EPI)) {
         acc += tc;
       } else if (EPI == kEpiStage) {
         __syncwarp();
@@ -1389,7 +1244,7 @@ __global__ void __launch_bounds__(kThreads,
     if (lane == 0 && ws) count_add(a, P.d[kc].count_out, ws);
   }
   C.flush(a.ctr, lane);
-  if (EPI == kEpiCount && a.mc_base) nvls_epilogue(P, warp, lane, s_wt);
+  if constexpr (EPI == kEpiCountMc) nvls_epilogue(P, warp, lane, s_wt);
 }
 
 }  // namespace smgpu

@@ -51,9 +51,7 @@ def test_plan_policy(sm):
     for c in b"ACGT":
         h[c] = 1000
     s, r = sm.sm_plan(b"ACGTACGTACGT", h)
-    # DNA: PACKED (2-bit codes); peel until alpha_eff x prod f <= 32 survivors per warp-block,
-    # which are then verified per lane: alpha_eff = 512, 512 * (1/4)^2 = 32
-    assert s == 4 and r == 2
+    assert s == 4 and r == 5                             # DNA: PACKED (2-bit codes); alpha_eff = 512, 512*(1/4)^5 = 1/2
     h2 = np.ones(256, dtype=np.uint64)
     s, r = sm.sm_plan(b"hello world", h2)
     assert s == sm.SM_STRATEGY_FILTER and r == 2        # phase B peels pi(1) and pi(2)

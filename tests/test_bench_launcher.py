@@ -80,3 +80,23 @@ def test_golden_check_catches_a_wrong_count():
     with pytest.raises(SystemExit):
         bench.golden_check("c1", bad, g["n"], len(want))
     assert bench.golden_check("c1", want, g["n"] + 1, len(want)) is None  # not the golden workload
+
+
+def test_reference_arm_under_torchrun_two_ranks():
+    """The driver's reference launch at N = 2 (torch.distributed.run, 127.0.0.1): rank 0
+    alone runs the oracle and prints ONE JSON line; rank 1 exits 0 without work."""
+    import json
+    env = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "bench.py"),
+           "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0", "--cpu-seconds", "1",
+           "--config", "c1"]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["config"]["world"] == 2
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["value"] > 0
