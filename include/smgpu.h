@@ -31,9 +31,9 @@
  *   - The caller owns every buffer; the library keeps no pointer after the
  *     call returns (async calls: after the enqueued work completes).
  *   - Scratch comes from the library's own stream-ordered memory pool per
- *     device (cudaMemPoolCreate; freed blocks stay cached up to
- *     SMGPU_POOL_KEEP_BYTES, default 1 GiB); the device's default pool is not
- *     touched.
+ *     device (cudaMemPoolCreate; freed blocks stay cached, up to
+ *     SMGPU_POOL_KEEP_BYTES if set, until sm_trim_scratch); the device's
+ *     default pool is not touched.
  *   - stream: a cudaStream_t passed as void*; NULL means cudaStreamPerThread.
  *
  * Errors: every call except sm_count returns sm_status and records it (with a
@@ -260,6 +260,12 @@ sm_status sm_last_error(void);
 const char* sm_last_error_message(void);
 void sm_clear_error(void);
 const char* sm_status_string(sm_status s);
+
+/* Return the library's cached scratch memory on the current device to the driver,
+ * keeping at most keep_bytes (0: all of it).  The pool caches freed per-call scratch
+ * (reporting staging up to 4 GiB, code arrays) so repeated calls cost no remapping;
+ * call this when that memory is needed elsewhere.  Synchronises the device. */
+sm_status sm_trim_scratch(size_t keep_bytes);
 
 /* Library version string and the number of kernels the library has launched
  * on this thread (for the benchmark's gpu_launches claim). */

@@ -44,7 +44,7 @@ STRATEGY_NAMES = {1: "filter", 2: "block", 3: "packed1", 4: "packed2", 5: "pair"
 EXPORTED_SYMBOLS = (
     "sm_count", "sm_report", "sm_symbol_order", "sm_histogram", "sm_order_from_histogram",
     "sm_count_async", "sm_count_batch", "sm_count_batch_ordered", "sm_count_batch_multicast", "sm_report_async", "sm_report_batch", "sm_heuristic_order", "sm_plan", "sm_last_error", "sm_last_error_message",
-    "sm_clear_error", "sm_status_string", "sm_version", "sm_launch_count", "sm_counters",
+    "sm_clear_error", "sm_status_string", "sm_version", "sm_launch_count", "sm_counters", "sm_trim_scratch",
 )
 COUNTER_NAMES = ("warp_tiles", "blocks", "steps", "filter_chunks", "filter_queued", "filter_survivors",
                  "filter_verify", "alpha_eff")
@@ -413,6 +413,16 @@ def sm_counters(reset: bool = False) -> dict:
     if s:
         _raise(s)
     return {k: int(v) for k, v in zip(COUNTER_NAMES, out)}
+
+
+def sm_trim_scratch(keep_bytes: int = 0) -> None:
+    """Hand the library's cached scratch memory on the current device back to the driver."""
+    lib = load_library()
+    lib.sm_trim_scratch.restype = ctypes.c_int
+    lib.sm_trim_scratch.argtypes = [_sz]
+    s = lib.sm_trim_scratch(int(keep_bytes))
+    if s != SM_OK:
+        _raise(s)
 
 
 def sm_version() -> str:

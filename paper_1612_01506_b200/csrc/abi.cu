@@ -167,6 +167,7 @@ struct Tunables {
   uint64_t dispatch_min_bytes = 64ull << 20;  // ... when the call streams at least this much text (n x P)
   uint64_t dispatch_min_bytes_single = 512ull << 20;  // single-pattern calls (the counter's memset
                                                       // costs more than it gains on short launches)
+  uint32_t list_max = 65535;    // reporting: a warp stages a u16 list for <= this many matches, else its bitmap
 };
 
 const Tunables& tunables() {
@@ -191,6 +192,7 @@ const Tunables& tunables() {
     if (const char* e = std::getenv("SMGPU_DISPATCH_MIN_MB")) x.dispatch_min_bytes = (uint64_t)std::atoll(e) << 20;
     if (const char* e = std::getenv("SMGPU_DISPATCH_MIN_MB_SINGLE"))
       x.dispatch_min_bytes_single = (uint64_t)std::atoll(e) << 20;
+    if (const char* e = std::getenv("SMGPU_LIST_MAX")) x.list_max = (uint32_t)std::atoi(e);
     if (x.ctas_pre < 1 || x.ctas_pre > 4) x.ctas_pre = 3;
     if (const char* e = std::getenv("SMGPU_STAGES_PRE")) x.max_stages_pre = (uint32_t)std::atoi(e);
     if (x.max_stages_pre < 2 || x.max_stages_pre > (uint32_t)kMaxStages) x.max_stages_pre = 6;
@@ -261,27 +263,30 @@ int text_code_bits(const uint64_t* hist, uint32_t* shift) {
 
 // Per-call scratch (report staging, code arrays, count cells) comes from the library's
 // own stream-ordered pool per device -- not the device's default pool, whose attributes
-// belong to the process.  Freed blocks stay cached up to SMGPU_POOL_KEEP_BYTES (default
-// 1 GiB) across synchronisations, so repeated calls cost no remapping; anything above is
-// returned to the driver at the next synchronisation.
+// belong to the process.  Freed blocks stay cached across synchronisations up to
+// SMGPU_POOL_KEEP_BYTES (default: all), so repeated calls cost no remapping (a 1 GiB cap
+// cost 12.5 ms per c2 report call: its 2-4 GiB staging pool was unmapped and remapped
+// every call, profiles/report_r2.md); sm_trim_scratch() hands the cached memory back.
 uint64_t pool_keep_bytes() {
   static const uint64_t v = [] {
     const char* e = std::getenv("SMGPU_POOL_KEEP_BYTES");
-    return e ? (uint64_t)std::strtoull(e, nullptr, 10) : (1ull << 30);
+    return e ? (uint64_t)std::strtoull(e, nullptr, 10) : UINT64_MAX;
   }();
   return v;
 }
+
+cudaMemPool_t g_pools[64] = {};
+std::mutex g_pool_mu;
 
 cudaError_t pool_alloc(void** ptr, size_t bytes, cudaStream_t st) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (dev < 0 || dev >= 64) return cudaMallocAsync(ptr, bytes, st);
-  static cudaMemPool_t pools[64] = {};
-  static std::mutex mu;
   cudaMemPool_t pool;
   {
-    std::lock_guard<std::mutex> g(mu);
+    std::lock_guard<std::mutex> g(g_pool_mu);
+    cudaMemPool_t* pools = g_pools;
     if (!pools[dev]) {
       cudaMemPoolProps props = {};
       props.allocType = cudaMemAllocationTypePinned;
@@ -791,7 +796,9 @@ uint64_t stage_pool_bytes(uint64_t cap, uint64_t items, uint64_t launches) {
     return e ? std::atoll(e) : -1LL;
   }();
   const uint64_t warps = (uint64_t)num_sms() * 4u * kConsumerWarps;  // >= resident compare warps
-  const uint64_t records = std::min<uint64_t>(16ull * cap, items * kConsumerWarps * 528ull);
+  // per position: <= 16 B as a list record; a bitmap record (528 B) holds > list_max of them
+  const uint64_t per_pos = std::max<uint64_t>(16, (528 + tunables().list_max) / (tunables().list_max + 1ull) + 16);
+  const uint64_t records = std::min<uint64_t>(per_pos * cap, items * kConsumerWarps * 528ull);
   const uint64_t partial = launches * warps * (uint64_t)kStageChunk * 16u;
   uint64_t b = env >= 0 ? (uint64_t)env : std::min<uint64_t>(4ull << 30, (64ull << 20) + records + partial);
   return (b + 15) & ~15ull;
@@ -832,132 +839,160 @@ sm_status enqueue_report_batch(const uint8_t* const* ps, const size_t* ms, size_
   CodeArray codes{prepack_text(h, t, n, P, false, st, &cb, &no_guard, &pe), st};
   if (pe != cudaSuccess) return cuda_fail(pe, "prepack");
   const TextInfo tinfo = text_info(h, n, P);
-  std::vector<Planned> plans;
-  plans.reserve(P);
+  const int epi1 = cap > 0 ? kEpiStage : kEpiCount;
+  // Patterns are planned in caller order and launched in strategy batches as soon as a
+  // batch is full, so the GPU starts while the host still orders later patterns.  Each
+  // pattern's work items get the slots [item_base, item_base + ntiles) of the per-item
+  // arrays, item_base = the prefix of the EARLIER patterns' tile counts (known when its
+  // batch launches), so one scan still yields the concatenated, pattern-ordered layout.
+  // The scratch is sized before the first launch with each pattern's largest possible
+  // tile count at the planned tile size.
+  const uint64_t T0 = tinfo.tiling.tile;
+  const uintptr_t tp = reinterpret_cast<uintptr_t>(t);
+  const uint64_t nt_max = ((tp & 15) + n + T0 - 1) / T0 + 2;
+  uint64_t items_max = 0;
+  for (size_t i = 0; i < P; ++i)
+    if (!(n < ms[i] || lim == 0)) items_max += nt_max;
+  if (items_max == 0) return SM_OK;
+  if (items_max >= (1ull << 31)) return fail(SM_EINVAL, "report: 2^31 or more (pattern, tile) work items in one call");
+  const uint64_t nL_max = (P + kMaxBatch - 1) / kMaxBatch + 16;  // typical launch count (+ slack)
+  size_t temp_bytes = 0;
+  SM_CUDA_TRY(exclusive_scan_wc(nullptr, nullptr, items_max, nullptr, &temp_bytes, st), "scan sizing");
+  auto al = [](uint64_t b) { return (b + 255) & ~255ull; };
+  uint8_t* scratch = nullptr;
+  uint16_t* wc = nullptr;
+  uint32_t *ovf_bits = nullptr, *ovf_n = nullptr, *ovf_items = nullptr;
+  unsigned long long *stage_used = nullptr, *expand_work = nullptr, *work = nullptr;
+  uint64_t* offsets = nullptr;
+  void* temp = nullptr;
+  uint8_t* stage = nullptr;
+  uint64_t stage_cap16 = 0;
+  const size_t max_launches = 2 * P + 16;  // every flush holds >= 1 pattern
+  cudaError_t e = cudaSuccess;
+  if (cap > 0) {
+    const uint64_t wc_b = al(items_max * 16), offs_b = al(items_max * 8), bits_b = al((items_max + 31) / 32 * 4),
+                   ovf_b = al(items_max * 4), ctr_b = al(16 + max_launches * 12), temp_b = al(temp_bytes),
+                   stage_b = stage_pool_bytes(cap, items_max, nL_max);
+    SM_CUDA_TRY(pool_alloc(reinterpret_cast<void**>(&scratch),
+                           wc_b + bits_b + ctr_b + offs_b + ovf_b + temp_b + stage_b, st),
+                "pool_alloc(report scratch)");
+    uint8_t* q = scratch;  // zero-initialised part first: wc, ovf_bits, counters
+    wc = reinterpret_cast<uint16_t*>(q); q += wc_b;
+    ovf_bits = reinterpret_cast<uint32_t*>(q); q += bits_b;
+    stage_used = reinterpret_cast<unsigned long long*>(q);
+    expand_work = stage_used + 1;
+    work = reinterpret_cast<unsigned long long*>(q + 16);  // [max_launches] pass-1 dispatch counters
+    ovf_n = reinterpret_cast<uint32_t*>(q + 16 + max_launches * 8); q += ctr_b;
+    offsets = reinterpret_cast<uint64_t*>(q); q += offs_b;
+    ovf_items = reinterpret_cast<uint32_t*>(q); q += ovf_b;
+    temp = q; q += temp_b;
+    stage = q;
+    // whole chunks only: every chunk a warp claims can hold the largest record plus its
+    // terminator, so no claimed chunk is ever left without a terminator header
+    stage_cap16 = stage_b / 16 / kStageChunk * kStageChunk;
+    e = cudaMemsetAsync(scratch, 0, wc_b + bits_b + ctr_b, st);
+    if (e != cudaSuccess) {
+      cudaFreeAsync(scratch, st);
+      return cuda_fail(e, "cudaMemsetAsync(report scratch)");
+    }
+  }
+  struct FreeScratch {
+    uint8_t* p;
+    cudaStream_t st;
+    ~FreeScratch() {
+      if (p) cudaFreeAsync(p, st);
+    }
+  } free_scratch{scratch, st};
+  const bool dispatch = use_dispatch(n, P);
+  std::vector<Planned> plans(P);
+  std::vector<std::vector<const Planned*>> runs;  // each launch's patterns (the overflow pass rebuilds)
+  std::vector<std::vector<uint64_t>> run_bases;   // and their item bases
+  std::vector<uint64_t> run_ovf;                  // and the offset of their overflow queue
+  std::vector<const Planned*> batch[8];
+  size_t words[8] = {};
+  uint64_t items = 0, ovf_at = 0;
+  std::vector<uint64_t> base_of(P, 0);
+  auto flush = [&](int strat) -> sm_status {
+    if (batch[strat].empty()) return SM_OK;
+    HostLaunch L;
+    build_launch(batch[strat], t, n, lim, epi1, L);
+    L.a.codes = codes.p;
+    std::vector<uint64_t> bases(L.d.size());
+    for (size_t k = 0; k < L.d.size(); ++k) {
+      const size_t i = (size_t)(L.d[k].count_out - d_counts);
+      if (L.d[k].ntiles > nt_max) return fail(SM_ENOMEM, "report: tile count bound exceeded");
+      L.d[k].item_base = base_of[i];
+      bases[k] = base_of[i];
+    }
+    run_ovf.push_back(ovf_at);
+    const size_t li = runs.size();
+    if (cap > 0) {
+      if (li >= max_launches) return fail(SM_ENOMEM, "report: launch count bound exceeded");
+      L.a.wc = wc;
+      L.a.stage = stage;
+      L.a.stage_used = stage_used;
+      L.a.stage_cap16 = stage_cap16;
+      L.a.ovf_bits = ovf_bits;
+      L.a.ovf_items = ovf_items + ovf_at;  // this launch's overflow queue (capacity: its items)
+      L.a.ovf_n = ovf_n + li;
+      L.a.pos_offset = pos_offset;
+      L.a.list_max = tunables().list_max;
+      if (dispatch && L.a.total_work < kNoItem) L.a.work_ctr = work + li;
+      ovf_at += L.a.total_work;
+    }
+    runs.push_back(batch[strat]);
+    run_bases.push_back(std::move(bases));
+    batch[strat].clear();
+    words[strat] = 0;
+    return launch_checked(L, st, cap > 0 ? "search kernel (report pass 1)" : "search kernel (report totals)");
+  };
   for (size_t i = 0; i < P; ++i) {
     if (n < ms[i] || lim == 0) continue;  // no alignments: count 0, no positions
-    Planned q{Plan(), ps[i], ms[i], d_counts + i};
+    Planned& q = plans[i];
+    q = Planned{Plan(), ps[i], ms[i], d_counts + i};
     sm_status s = make_plan(ps[i], ms[i], n, h, P == 1 ? order : nullptr, P == 1 ? peel : 0, strategy, q.pl,
                             &tinfo);
     if (s != SM_OK) return s;
     use_codes(codes, cb, q.pl);
-    plans.push_back(std::move(q));
-  }
-  if (plans.empty()) return SM_OK;
-  const int epi1 = cap > 0 ? kEpiStage : kEpiCount;
-  // launches grouped by strategy (batch limits as for counting); every pattern keeps
-  // a fixed slot range [item_base, item_base + ntiles) of the per-tile arrays in the
-  // caller's order, so one scan gives the concatenated, pattern-ordered output layout
-  std::vector<HostLaunch> Ls;
-  std::vector<std::vector<const Planned*>> runs;  // each launch's patterns (the overflow pass rebuilds)
-  for (int strat : {(int)kFilter, (int)kPair, (int)kBlock, (int)kPacked1, (int)kPacked2, (int)kPacked1Pre,
-                    (int)kPacked2Pre}) {
-    std::vector<const Planned*> run;
-    size_t words = 0;
-    auto flush = [&]() {
-      if (run.empty()) return;
-      Ls.emplace_back();
-      build_launch(run, t, n, lim, epi1, Ls.back());
-      Ls.back().a.codes = codes.p;
-      runs.push_back(run);
-      run.clear();
-      words = 0;
-    };
-    for (const Planned& q : plans) {
-      if (q.pl.strategy != strat) continue;
-      if (run.size() == (size_t)kMaxBatch || words + table_words(q) > (size_t)kBatchTableWords) flush();
-      run.push_back(&q);
-      words += table_words(q);
-    }
-    flush();
-  }
-  if (cap == 0) {  // totals only
-    for (HostLaunch& L : Ls) {
-      sm_status s = launch_checked(L, st, "search kernel (report totals)");
+    PatDesc d;  // this pattern's tile count at the launch tile size (fill_desc is what build_launch uses)
+    fill_desc(q.pl, q.p, q.m, tp & 15, n, lim, T0, d, 0);
+    if (d.ntiles > nt_max) return fail(SM_ENOMEM, "report: tile count bound exceeded");
+    base_of[i] = items;
+    items += nt_max;  // slots [base, base + ntiles) used; the rest of the pattern's slots stay zero
+    const int k = q.pl.strategy;
+    if (batch[k].size() == (size_t)kMaxBatch || words[k] + table_words(q) > (size_t)kBatchTableWords) {
+      s = flush(k);
       if (s != SM_OK) return s;
     }
-    return SM_OK;
+    batch[k].push_back(&q);
+    words[k] += table_words(q);
   }
-  // item bases in pattern order (a descriptor's pattern index = its count_out - d_counts)
-  std::vector<PatDesc*> slot(P, nullptr);
-  for (HostLaunch& L : Ls)
-    for (PatDesc& d : L.d) slot[(size_t)(d.count_out - d_counts)] = &d;
-  uint64_t items = 0;
-  for (size_t i = 0; i < P; ++i)
-    if (slot[i]) {
-      slot[i]->item_base = items;
-      items += slot[i]->ntiles;
-    }
-  if (items >= (1ull << 31)) return fail(SM_EINVAL, "report: 2^31 or more (pattern, tile) work items in one call");
-  size_t temp_bytes = 0;
-  SM_CUDA_TRY(exclusive_scan_wc(nullptr, nullptr, items, nullptr, &temp_bytes, st), "scan sizing");
-  auto al = [](uint64_t b) { return (b + 255) & ~255ull; };
-  const uint64_t nL = Ls.size();
-  const uint64_t wc_b = al(items * 16), offs_b = al(items * 8), bits_b = al((items + 31) / 32 * 4),
-                 ovf_b = al(items * 4), ctr_b = al(16 + nL * 12), temp_b = al(temp_bytes),
-                 stage_b = stage_pool_bytes(cap, items, nL);
-  uint8_t* scratch = nullptr;
-  SM_CUDA_TRY(pool_alloc(reinterpret_cast<void**>(&scratch),
-                              wc_b + bits_b + ctr_b + offs_b + ovf_b + temp_b + stage_b, st),
-              "pool_alloc(report scratch)");
-  uint8_t* q = scratch;  // zero-initialised part first: wc, ovf_bits, counters
-  uint16_t* wc = reinterpret_cast<uint16_t*>(q); q += wc_b;
-  uint32_t* ovf_bits = reinterpret_cast<uint32_t*>(q); q += bits_b;
-  unsigned long long* stage_used = reinterpret_cast<unsigned long long*>(q);
-  unsigned long long* expand_work = stage_used + 1;
-  unsigned long long* work = reinterpret_cast<unsigned long long*>(q + 16);  // [nL] pass-1 dispatch counters
-  uint32_t* ovf_n = reinterpret_cast<uint32_t*>(q + 16 + nL * 8); q += ctr_b;
-  const bool dispatch = use_dispatch(n, P);
-  uint64_t* offsets = reinterpret_cast<uint64_t*>(q); q += offs_b;
-  uint32_t* ovf_items = reinterpret_cast<uint32_t*>(q); q += ovf_b;
-  void* temp = q; q += temp_b;
-  uint8_t* stage = q;
-  cudaError_t e = cudaMemsetAsync(scratch, 0, wc_b + bits_b + ctr_b, st);
-  // whole chunks only: every chunk a warp claims can hold the largest record plus its
-  // terminator, so no claimed chunk is ever left without a terminator header
-  const uint64_t stage_cap16 = stage_b / 16 / kStageChunk * kStageChunk;
-  uint64_t ovf_at = 0;
-  for (size_t li = 0; li < Ls.size(); ++li) {  // pass 1: per-warp counts + staged records
-    if (e != cudaSuccess) break;
-    HostLaunch& L = Ls[li];
-    L.a.wc = wc;
-    L.a.stage = stage;
-    L.a.stage_used = stage_used;
-    L.a.stage_cap16 = stage_cap16;
-    L.a.ovf_bits = ovf_bits;
-    L.a.ovf_items = ovf_items + ovf_at;  // this launch's overflow queue (capacity: its items)
-    L.a.ovf_n = ovf_n + li;
-    L.a.pos_offset = pos_offset;
-    if (dispatch && L.a.total_work < kNoItem) L.a.work_ctr = work + li;
-    ovf_at += L.a.total_work;
-    e = launch_search(L, st);
-    if (e == cudaSuccess) ++g_launches;
+  for (int k = 1; k < 8; ++k) {
+    sm_status s = flush(k);
+    if (s != SM_OK) return s;
   }
-  if (e == cudaSuccess) {
-    e = exclusive_scan_wc(wc, offsets, items, temp, &temp_bytes, st);
-    if (e == cudaSuccess) g_launches += 1;
-  }
+  if (cap == 0 || runs.empty()) return SM_OK;
+  e = exclusive_scan_wc(wc, offsets, items, temp, &temp_bytes, st);
+  if (e == cudaSuccess) g_launches += 1;
   if (e == cudaSuccess) {
     e = launch_stage_expand(stage, stage_used, stage_cap16, wc, offsets, pos, cap, expand_work, num_sms(), st);
     if (e == cudaSuccess) ++g_launches;
   }
-  for (size_t li = 0; li < Ls.size(); ++li) {  // overflow pass (CTAs exit at once when the queue is empty)
+  for (size_t li = 0; li < runs.size(); ++li) {  // overflow pass (CTAs exit at once when the queue is empty)
     if (e != cudaSuccess) break;
     HostLaunch W;  // its own shared-memory layout (position lists), same patterns and arguments
     build_launch(runs[li], t, n, lim, kEpiWrite, W);
-    for (size_t i = 0; i < W.d.size(); ++i) W.d[i].item_base = Ls[li].d[i].item_base;
-    const LaunchArgs& a1 = Ls[li].a;
-    W.a.codes = a1.codes;
-    W.a.ovf_items = a1.ovf_items;
-    W.a.ovf_n = a1.ovf_n;
-    W.a.pos_offset = a1.pos_offset;
+    for (size_t i = 0; i < W.d.size(); ++i) W.d[i].item_base = run_bases[li][i];
+    W.a.codes = codes.p;
+    W.a.ovf_items = ovf_items + run_ovf[li];
+    W.a.ovf_n = ovf_n + li;
+    W.a.pos_offset = pos_offset;
     W.a.tile_offsets = offsets;
     W.a.pos = pos;
     W.a.cap = cap;
     e = launch_search(W, st);
     if (e == cudaSuccess) ++g_launches;
   }
-  cudaFreeAsync(scratch, st);
   if (e != cudaSuccess) return cuda_fail(e, "report");
   return SM_OK;
 }
@@ -1274,6 +1309,20 @@ sm_status sm_counters(uint64_t* out, int reset) {
   SM_CUDA_TRY(cudaDeviceSynchronize(), "sm_counters sync");
   SM_CUDA_TRY(cudaMemcpy(out, d, kCounters * sizeof(uint64_t), cudaMemcpyDeviceToHost), "sm_counters copy");
   if (reset) SM_CUDA_TRY(cudaMemset(d, 0, kCounters * sizeof(uint64_t)), "sm_counters reset");
+  return SM_OK;
+}
+
+sm_status sm_trim_scratch(size_t keep_bytes) {
+  int dev = 0;
+  SM_CUDA_TRY(cudaGetDevice(&dev), "cudaGetDevice");
+  cudaMemPool_t pool = nullptr;
+  {
+    std::lock_guard<std::mutex> g(g_pool_mu);
+    if (dev >= 0 && dev < 64) pool = g_pools[dev];
+  }
+  if (!pool) return SM_OK;  // nothing allocated on this device yet
+  SM_CUDA_TRY(cudaDeviceSynchronize(), "sm_trim_scratch sync");
+  SM_CUDA_TRY(cudaMemPoolTrimTo(pool, keep_bytes), "cudaMemPoolTrimTo");
   return SM_OK;
 }
 

@@ -48,17 +48,23 @@ __host__ __device__ constexpr bool is_count_epi(int e) { return e == kEpiCount |
 // 16-B units per chunk, grabbed with one global atomic; records packed back to back,
 // a zero header terminates a chunk's records):
 //   header (16 B): i64 pos_base (0-based position of tile-relative alignment u = 0,
-//                  shard offset included), u32 item, u16 cnt, u8 warp, u8 log2(CPL);
-//   data: when 2 cnt < wspan / 8 (wspan = 512 CPL alignments per warp) the ascending
-//         u16 list of the tile-relative alignments u (padded to 16 B), else the warp's
-//         bitmap, wspan / 16 u16 words, bit b of word i <-> u = warp wspan + 16 i + b.
+//                  shard offset included), u32 item, u16 cnt, u8 warp, then bits 24-25
+//                  log2(CPL) and bit 31 = bitmap record;
+//   data: a list record (cnt <= list_max and 2 cnt < wspan / 8, wspan = 512 CPL
+//         alignments per warp) holds the ascending u16 list of the tile-relative
+//         alignments u (padded to 16 B); a bitmap record the warp's bitmap, wspan / 16
+//         u16 words, bit b of word i <-> u = warp wspan + 16 i + b.
 // and posts cnt into wc[item][warp] (u16 x 8 per item, zero-initialised): the scan of
 // the per-item sums gives each item's output offset, wc its warps' order inside it.
 constexpr uint32_t kRecHeader = 16;
 constexpr uint32_t kStageChunk = 512;   // 16-B units (8 KiB) >= largest record (528 B) + terminator
-__host__ __device__ inline uint32_t rec_warp_bytes(uint32_t cnt, uint32_t wspan) {
+constexpr uint32_t kRecBitmap = 1u << 31;  // header word 3: bitmap record
+__host__ __device__ inline bool rec_is_list(uint32_t cnt, uint32_t wspan, uint32_t list_max) {
+  return cnt <= list_max && 2u * cnt < wspan / 8u;
+}
+__host__ __device__ inline uint32_t rec_data_bytes(uint32_t cnt, uint32_t wspan, bool list) {
   if (cnt == 0) return 0;
-  return 2u * cnt < wspan / 8u ? ((2u * cnt + 15u) & ~15u) : wspan / 8u;
+  return list ? ((2u * cnt + 15u) & ~15u) : wspan / 8u;
 }
 
 // One pattern of a launch.  Byte offsets are relative to `base` = align_down(t, 16);
@@ -118,6 +124,7 @@ struct LaunchArgs {
   uint64_t* pos;             // kEpiWrite: output positions
   uint64_t cap;              // kEpiWrite: capacity of pos
   uint64_t pos_offset;       // kEpiStage / kEpiWrite: added to every position (a shard's first owned position)
+  uint32_t list_max;         // kEpiStage: a warp with at most this many matches stages a list record, more a bitmap
   unsigned long long* ctr;   // instrumented build (SMGPU_COUNTERS) only: device u64[kCounters], else unused
   unsigned long long* work_ctr;  // count / stage: non-null = work items are dispatched from this zeroed
                                  // counter (the producer fetches, the consumers read the stage's item)

@@ -932,7 +932,8 @@ __device__ __forceinline__ void stage_warp(const LaunchArgs& a, uint16_t* bm, St
                                            int warp, int lane, uint64_t item, int64_t pos_base, uint32_t wcnt) {
   constexpr uint32_t kWspan = 512u * CPL;  // alignments per warp (32 lanes x CPL chunks x 16)
   constexpr uint32_t kLog2Cpl = CPL == 8 ? 3 : CPL == 4 ? 2 : CPL == 2 ? 1 : 0;
-  const uint32_t dbytes = rec_warp_bytes(wcnt, kWspan);
+  const bool as_list = rec_is_list(wcnt, kWspan, a.list_max);
+  const uint32_t dbytes = rec_data_bytes(wcnt, kWspan, as_list);
   unsigned long long o = 0;
   if (lane == 0) {
     a.wc[item * kConsumerWarps + warp] = (uint16_t)wcnt;  // (the pattern total: the caller's acc)
@@ -948,11 +949,11 @@ __device__ __forceinline__ void stage_warp(const LaunchArgs& a, uint16_t* bm, St
       h.x = (uint32_t)(uint64_t)pos_base;
       h.y = (uint32_t)((uint64_t)pos_base >> 32);
       h.z = (uint32_t)item;
-      h.w = wcnt | ((uint32_t)warp << 16) | (kLog2Cpl << 24);
+      h.w = wcnt | ((uint32_t)warp << 16) | (kLog2Cpl << 24) | (as_list ? 0u : kRecBitmap);
       reinterpret_cast<uint4*>(rec)[0] = h;
       reinterpret_cast<uint4*>(rec + kRecHeader + dbytes)[0] = make_uint4(0u, 0u, 0u, 0u);  // terminator
     }
-    if (2u * wcnt < kWspan / 8u) {  // sparse: ascending u16 list (lane l owns chunks [l CPL, l CPL + CPL))
+    if (as_list) {  // sparse: ascending u16 list (lane l owns chunks [l CPL, l CPL + CPL))
       uint16_t mk[CPL];
       uint32_t pc = 0;
 #pragma unroll

@@ -33,9 +33,8 @@ __device__ __forceinline__ uint32_t warp_incl_scan_x(uint32_t v, int lane) {
   return v;
 }
 
-__device__ __forceinline__ bool is_list_record(uint32_t hw) {
-  return 2u * (hw & 0xFFFFu) < (512u << (hw >> 24)) / 8u;  // 2 count < wspan / 8
-}
+__device__ __forceinline__ bool is_list_record(uint32_t hw) { return (hw & kRecBitmap) == 0u; }
+__device__ __forceinline__ uint32_t rec_wspan(uint32_t hw) { return 512u << ((hw >> 24) & 3u); }
 
 // a bitmap record: bit b of u32 word i <-> u = w wspan + 32 i + b
 __device__ __forceinline__ void write_bitmap(const uint8_t* rec, uint64_t out, uint64_t* pos, uint64_t cap,
@@ -43,7 +42,7 @@ __device__ __forceinline__ void write_bitmap(const uint8_t* rec, uint64_t out, u
   const uint4 h = *reinterpret_cast<const uint4*>(rec);
   const int64_t pos_base = (int64_t)(((uint64_t)h.y << 32) | h.x);
   const uint32_t w = (h.w >> 16) & 0xFFu;
-  const uint32_t wspan = 512u << (h.w >> 24);
+  const uint32_t wspan = rec_wspan(h.w);
   const uint8_t* data = rec + kRecHeader;
   const uint32_t* bm = reinterpret_cast<const uint32_t*>(data);
   const uint32_t words = wspan / 32u;
@@ -131,7 +130,7 @@ __global__ void __launch_bounds__(kExpandWarps * 32, 2) stage_expand_kernel(cons
         const uint32_t c = hw & 0xFFFFu;
         if (c == 0) break;
         roff[nrec++] = (uint16_t)o;
-        o += 1u + rec_warp_bytes(c, 512u << (hw >> 24)) / 16u;
+        o += 1u + rec_data_bytes(c, rec_wspan(hw), is_list_record(hw)) / 16u;
       }
     }
     nrec = __shfl_sync(0xFFFFFFFFu, nrec, 0);

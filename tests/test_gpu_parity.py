@@ -539,3 +539,22 @@ def test_caller_histogram_matching_text_keeps_packed(sm):
     sm.sm_count_batch(pats, t, d0)
     want = [oracle.naive_count(p, a) for p in pats]
     assert d.cpu().tolist() == want and d0.cpu().tolist() == want
+
+
+def test_trim_scratch_then_report(sm):
+    """sm_trim_scratch hands the cached scratch back; the next report re-allocates it and
+    still equals the oracle (and a report right after another reuses the cached pool)."""
+    rng = np.random.default_rng(5)
+    a = np.frombuffer(b"ab ", dtype=np.uint8)[rng.integers(0, 3, 300_001)].copy()
+    t = dev(a, 3)
+    pats = [b"ab", b"a b", b" ", b"bba"]
+    want = [oracle.naive_count(p, a) for p in pats]
+    wp = np.concatenate([oracle.naive_report(p, a) for p in pats])
+    for trim in (False, True, False):
+        if trim:
+            sm.sm_trim_scratch(0)
+        pos = torch.zeros(int(sum(want)), dtype=torch.int64, device="cuda")
+        d = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
+        sm.sm_report_batch(pats, t, pos, d)
+        assert d.cpu().tolist() == want
+        assert np.array_equal(pos.cpu().numpy().astype(np.uint64), wp.astype(np.uint64))

@@ -47,6 +47,7 @@ def main():
     ap.add_argument("--lengths", default="4,8,16,32,64")
     ap.add_argument("--per-m", type=int, default=16)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--rmax", type=int, default=8)
     a = ap.parse_args()
     torch.cuda.set_device(0)
     for cfg in a.configs.split(","):
@@ -74,7 +75,7 @@ def main():
                 strat = sm.SM_STRATEGY_PACKED if packed else sm.SM_STRATEGY_BLOCK
                 sname = "packed" if packed else "block"
                 variants.append(("auto", None, None, 0))
-                for r in range(1, 9):
+                for r in range(1, a.rmax + 1):
                     variants.append((f"{sname}/r={r}", None, [r] * len(ps), strat))
                 row["auto_plan"] = [sm.STRATEGY_NAMES[x] + f"/r={y}" for x, y in [sm.sm_plan(ps[0], hist)]]
             for name, orders, peels, strat in variants:
