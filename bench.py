@@ -2,7 +2,8 @@
 """Benchmark: text GB/s scanned per pattern (device-timed), % of B200 HBM peak.
 
 One STEP = one pass of the whole hot path over the config's synthetic text:
-  A1  device histogram of the (owned) text  [+ NCCL all_reduce for N > 1]
+  A1  device histogram of the (owned) text (N = 1: inside sm_count_batch; N > 1: by the
+      bench, + NCCL all_reduce, so every rank uses the same order)
   A2  rarest-first order pi per pattern (host, from the histogram)
   A3-A7 one counting search launch per pattern (TMA staging, peeled packed-byte
       compares, early exit, popcount/atomics)          [+ all_reduce of counts]
@@ -409,7 +410,18 @@ def run_native(args):
     fused = bool(mc is not None and mc.available)
 
     def step(ev=None):
-        h = smd.global_histogram(text, shard)             # A1 (+ all_reduce)
+        if world == 1:
+            # A1 inside the call: the library histograms t itself (its own, trusted histogram:
+            # no device support check / fallback launches for PACKED, R21), then A2..A7
+            if ev is not None:
+                ev[0].record(stream)
+            sm.sm_count_batch(pbatch, held, counts, hist=None, max_alignments=shard.owned_bytes,
+                              strategy=args.strategy)
+            if ev is not None:
+                ev[1].record(stream)
+                ev[2].record(stream)
+            return None
+        h = smd.global_histogram(text, shard)             # A1 (+ all_reduce: one pi on every rank, R14)
         hh = h.cpu().numpy().astype(np.uint64)           # 2 KiB D2H for the host-side order (A2)
         if ev is not None:
             ev[0].record(stream)
@@ -436,8 +448,10 @@ def run_native(args):
         torch.cuda.synchronize()
 
     for _ in range(max(args.warmup, 1)):
-        hh = step()
+        step()
     barrier()
+    # the text's histogram for the diagnostics below (plans, per-length passes): outside the timed region
+    hh = smd.global_histogram(text, shard).cpu().numpy().astype(np.uint64)
 
     # ---------------- timed region (device time, max over ranks)
     clk = ClockSampler(local)
@@ -522,8 +536,9 @@ def run_native(args):
             b = i % 2
             stream.wait_event(copied[b])
             held_b = bufs[b][: shard.held_len]
-            h = smd.global_histogram(bufs[b], shard)
-            hh2 = h.cpu().numpy().astype(np.uint64)
+            hh2 = None  # N = 1: the library histograms the text itself (as in the timed step)
+            if world > 1:
+                hh2 = smd.global_histogram(bufs[b], shard).cpu().numpy().astype(np.uint64)
             sm.sm_count_batch(pbatch, held_b, counts, hist=hh2, max_alignments=shard.owned_bytes)
             consumed[b].record(stream)
             smd.allreduce_sum_(counts)

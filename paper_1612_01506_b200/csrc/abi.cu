@@ -2,6 +2,7 @@
 // peeling factor r, strategy, tiling) and launch orchestration.  Host code only;
 // every step of the path on the text runs in the kernels of this library.
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cmath>
 #include <cstdio>
@@ -657,6 +658,37 @@ sm_status launch_checked(const HostLaunch& L, cudaStream_t st, const char* what)
 // Counts of P patterns over one text in as few launches as the batch limits allow
 // (each launch runs every one of its patterns as a full pass over the text).
 // order / peel: the caller's comparison order and peeling factor (P == 1 only).
+// Host-side phase timing of one count call (SMGPU_HOST_TIMING=1: one line per call on
+// stderr, microseconds) -- for the small-text regime where the host enqueue bounds the
+// step (c1).
+struct HostTiming {
+  using clk = std::chrono::steady_clock;
+  bool on;
+  clk::time_point t0, last;
+  double prep = 0, plan = 0, build = 0, launch = 0;
+  int launches = 0;
+  HostTiming() {
+    static const bool enabled = [] {
+      const char* e = std::getenv("SMGPU_HOST_TIMING");
+      return e && std::atoi(e) != 0;
+    }();
+    on = enabled;
+    if (on) t0 = last = clk::now();
+  }
+  double lap() {
+    const auto now = clk::now();
+    const double us = std::chrono::duration<double, std::micro>(now - last).count();
+    last = now;
+    return us;
+  }
+  void report(size_t P) {
+    if (!on) return;
+    const double tot = std::chrono::duration<double, std::micro>(clk::now() - t0).count();
+    std::fprintf(stderr, "smgpu host: P=%zu total=%.1f prep=%.1f plan=%.1f build=%.1f launch=%.1f launches=%d\n", P,
+                 tot, prep, plan, build, launch, launches);
+  }
+};
+
 // orders / peels: the caller's comparison orders (concatenated, m[i] entries each) and
 // peeling factors (0 = auto), or nullptr for the rarest-first order / auto r.
 // mc / done (NEXT-4): every launch also adds its patterns' counts to mc[i] through the
@@ -666,6 +698,7 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
                               cudaStream_t st, const uint32_t* orders = nullptr, const uint32_t* peels = nullptr,
                               uint64_t* mc = nullptr, unsigned int* done = nullptr) {
   if (P == 0) return SM_OK;
+  HostTiming ht;
   SM_CUDA_TRY(cudaMemsetAsync(d_counts, 0, P * sizeof(uint64_t), st), "cudaMemsetAsync(counts)");
   uint64_t hb[256];
   const uint64_t* h = hist;
@@ -708,12 +741,14 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
     }
   } free_work{work, st};
   size_t used_done = 0;
+  if (ht.on) ht.prep += ht.lap();
   std::vector<Planned> plans(P), fallback(guard ? P : 0);
   constexpr int kStrategies = 8;                  // index = strategy value (1..7)
   std::vector<const Planned*> batch[2][kStrategies];  // [0]: plans, [1]: guarded fallbacks
   size_t words[2][kStrategies] = {};
   auto flush = [&](int fb, int strat) -> sm_status {
     if (batch[fb][strat].empty()) return SM_OK;
+    if (ht.on) ht.plan += ht.lap();
     HostLaunch L;
     build_launch(batch[fb][strat], t, n, lim, mc ? kEpiCountMc : kEpiCount, L);
     L.a.codes = codes.p;
@@ -734,7 +769,13 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
     }
     batch[fb][strat].clear();
     words[fb][strat] = 0;
-    return launch_checked(L, st, fb ? "search kernel (guarded fallback)" : "search kernel (batch)");
+    if (ht.on) ht.build += ht.lap();
+    const sm_status ls = launch_checked(L, st, fb ? "search kernel (guarded fallback)" : "search kernel (batch)");
+    if (ht.on) {
+      ht.launch += ht.lap();
+      ++ht.launches;
+    }
+    return ls;
   };
   auto add = [&](int fb, const Planned& q) -> sm_status {
     const int k = q.pl.strategy;
@@ -772,6 +813,7 @@ sm_status enqueue_count_batch(const uint8_t* const* ps, const size_t* ms, size_t
       sm_status s = flush(fb, k);
       if (s != SM_OK) return s;
     }
+  ht.report(P);
   return SM_OK;
 }
 
