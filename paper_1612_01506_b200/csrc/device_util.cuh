@@ -162,6 +162,14 @@ __device__ __forceinline__ uint32_t eq_flags_raw(uint32_t w, uint32_t bc) {
   uint32_t t = (y & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;  // bit7 set iff low 7 bits nonzero
   return ~(t | y);                              // bit7 set iff y byte == 0
 }
+// eq_flags_raw with its add as an IMAD (k1 = 1, opaque to the compiler: a value the caller
+// derives from a kernel parameter): the byte compares are ALU-pipe bound, the FMA pipe idles
+__device__ __forceinline__ uint32_t eq_flags_fma(uint32_t w, uint32_t bc, uint32_t k1) {
+  const uint32_t y = w ^ bc;
+  uint32_t t;
+  asm("mad.lo.u32 %0, %1, %2, 0x7F7F7F7F;" : "=r"(t) : "r"(y & 0x7F7F7F7Fu), "r"(k1));
+  return ~(t | y);
+}
 // "any byte equal" test term (exact as a whole-word predicate; per-byte bits may
 // include false positives above a true match, so it is only ever OR-reduced)
 __device__ __forceinline__ uint32_t any_eq_term(uint32_t w, uint32_t bc) {

@@ -61,12 +61,23 @@ __device__ __forceinline__ uint4 window16_q(const uint8_t* base16, uint32_t sh) 
                     byte_window(w[Q + 2], w[Q + 3], sh), byte_window(w[Q + 3], w[Q + 4], sh));
 }
 
+// y - 0x01010101 (the borrow term of the zero-byte test) as an IMAD, k = 1 opaque to the
+// compiler: phase A's chunk tests are ALU-pipe bound (LOP3 / SHF / IADD3), the FMA pipe idles
+// (FILTER c5 and PAIR c3 m = 16: ALU pipe 76-79 %; under the pool's sustained power cap the SM
+// clock falls to ~1.5 GHz and the ALU pipe, not HBM, sets the rate)
+__device__ __forceinline__ uint32_t borrow_fma(uint32_t y, uint32_t k1) {
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, 0xFEFEFEFF;" : "=r"(r) : "r"(y), "r"(k1));
+  return r;
+}
+
 // found &= SIMDcompare(...) for the 16 alignments whose compared bytes are `w`
-__device__ __forceinline__ void found_and_eq(Found4& F, const uint4 w, uint32_t bc) {
-  F.f0 &= eq_flags_raw(w.x, bc);
-  F.f1 &= eq_flags_raw(w.y, bc);
-  F.f2 &= eq_flags_raw(w.z, bc);
-  F.f3 &= eq_flags_raw(w.w, bc);
+// (k1 = 1 opaque, see eq_flags_fma)
+__device__ __forceinline__ void found_and_eq(Found4& F, const uint4 w, uint32_t bc, uint32_t k1) {
+  F.f0 &= eq_flags_fma(w.x, bc, k1);
+  F.f1 &= eq_flags_fma(w.y, bc, k1);
+  F.f2 &= eq_flags_fma(w.z, bc, k1);
+  F.f3 &= eq_flags_fma(w.w, bc, k1);
 }
 
 __device__ __forceinline__ Found4 found_all() { return Found4{0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u}; }
@@ -263,8 +274,11 @@ __device__ void produce(const LaunchParams<CAP>& P, uint8_t* ring, uint64_t* ful
 
 // FILTER phase A: does any of the 16 pi(1)-bytes of a chunk equal p[pi(1)]?
 // (borrow-based zero-byte test: exact as a whole-chunk predicate)
-__device__ __forceinline__ bool chunk_hit(const uint4 v, uint32_t bc) {
-  return ((any_eq_term(v.x, bc) | any_eq_term(v.y, bc) | any_eq_term(v.z, bc) | any_eq_term(v.w, bc)) &
+// (k1 = 1, see borrow_fma)
+__device__ __forceinline__ bool chunk_hit(const uint4 v, uint32_t bc, uint32_t k1) {
+  const uint32_t y0 = v.x ^ bc, y1 = v.y ^ bc, y2 = v.z ^ bc, y3 = v.w ^ bc;
+  return (((borrow_fma(y0, k1) & ~y0) | (borrow_fma(y1, k1) & ~y1) | (borrow_fma(y2, k1) & ~y2) |
+           (borrow_fma(y3, k1) & ~y3)) &
           0x80808080u) != 0;
 }
 
@@ -293,13 +307,13 @@ __device__ __forceinline__ void pair_windows(const uint8_t* buf, uint32_t c, uin
 
 template <int QA, bool WORD_ALIGNED = false>
 __device__ __forceinline__ bool pair_hit(const uint8_t* buf, uint32_t c, uint32_t pre, uint32_t s2, uint32_t bc1,
-                                         uint32_t bc2) {
+                                         uint32_t bc2, uint32_t k1) {
   uint4 v1, v2;
   pair_windows<QA, WORD_ALIGNED>(buf, c, pre, s2, v1, v2);
   const uint32_t y0 = (v1.x ^ bc1) | (v2.x ^ bc2), y1 = (v1.y ^ bc1) | (v2.y ^ bc2);
   const uint32_t y2 = (v1.z ^ bc1) | (v2.z ^ bc2), y3 = (v1.w ^ bc1) | (v2.w ^ bc2);
-  return ((((y0 - 0x01010101u) & ~y0) | ((y1 - 0x01010101u) & ~y1) | ((y2 - 0x01010101u) & ~y2) |
-           ((y3 - 0x01010101u) & ~y3)) &
+  return (((borrow_fma(y0, k1) & ~y0) | (borrow_fma(y1, k1) & ~y1) | (borrow_fma(y2, k1) & ~y2) |
+           (borrow_fma(y3, k1) & ~y3)) &
           0x80808080u) != 0;
 }
 
@@ -329,10 +343,11 @@ template <int Q>
 __device__ __forceinline__ uint32_t filter_entry(const Pat& pt, const uint8_t* buf, uint32_t c, bool edge,
                                                  int32_t rlo, int32_t rhi) {
   Found4 F = edge ? found_from_mask16(range_mask16_rel((int32_t)(16u * c), rlo, rhi)) : found_all();
-  found_and_eq(F, lds128(buf + pt.pre + 16u * c), pt.bc1);  // pi(1)
+  const uint32_t k1 = 1u + (pt.m >> 31);
+  found_and_eq(F, lds128(buf + pt.pre + 16u * c), pt.bc1, k1);  // pi(1)
   SMGPU_DCHECK(pt.m < 2 || 16u * c + (pt.s2 & ~15u) + 32u <= pt.lim);
   if (pt.m >= 2)                                               // pi(2)
-    found_and_eq(F, window16_q<Q>(buf + 16u * c + (pt.s2 & ~15u), (pt.s2 & 3u) * 8u), pt.bc2);
+    found_and_eq(F, window16_q<Q>(buf + 16u * c + (pt.s2 & ~15u), (pt.s2 & 3u) * 8u), pt.bc2, k1);
   return compress_found(F);
 }
 
@@ -480,6 +495,7 @@ __device__ __forceinline__ void filter_tile_q(const Pat& pt, const uint8_t* buf,
                                               bool edge, int32_t rlo, int32_t rhi, Sink& sink, Ctr& C) {
   C.add(kCtrChunks, 32u * CPL);
   if constexpr (PA) {
+    const uint32_t k1 = 1u + (pt.m >> 31);  // 1, opaque (eq_flags_fma)
     if (pt.m == 2) {  // warp-uniform: pi(1), pi(2) are the whole pattern, so the pair test of
                       // phase A, taken per byte, IS the match -- one pass, no queue, no phase B
 #pragma unroll
@@ -489,10 +505,10 @@ __device__ __forceinline__ void filter_tile_q(const Pat& pt, const uint8_t* buf,
         uint4 v1, v2;
         pair_windows<QA, WA>(buf, c, pt.pre, pt.s2, v1, v2);
         Found4 F = edge ? found_from_mask16(range_mask16_rel((int32_t)(16u * c), rlo, rhi)) : found_all();
-        F.f0 &= eq_flags_raw((v1.x ^ pt.bc1) | (v2.x ^ pt.bc2), 0u);
-        F.f1 &= eq_flags_raw((v1.y ^ pt.bc1) | (v2.y ^ pt.bc2), 0u);
-        F.f2 &= eq_flags_raw((v1.z ^ pt.bc1) | (v2.z ^ pt.bc2), 0u);
-        F.f3 &= eq_flags_raw((v1.w ^ pt.bc1) | (v2.w ^ pt.bc2), 0u);
+        F.f0 &= eq_flags_fma((v1.x ^ pt.bc1) | (v2.x ^ pt.bc2), 0u, k1);
+        F.f1 &= eq_flags_fma((v1.y ^ pt.bc1) | (v2.y ^ pt.bc2), 0u, k1);
+        F.f2 &= eq_flags_fma((v1.z ^ pt.bc1) | (v2.z ^ pt.bc2), 0u, k1);
+        F.f3 &= eq_flags_fma((v1.w ^ pt.bc1) | (v2.w ^ pt.bc2), 0u, k1);
         const uint32_t g = compress_found(F);
         C.add(kCtrSurvivors, __popc(g));
         sink(c, g, lane);
@@ -501,6 +517,7 @@ __device__ __forceinline__ void filter_tile_q(const Pat& pt, const uint8_t* buf,
     }
   }
   constexpr int G = CPL < kGroup ? CPL : kGroup;
+  const uint32_t k1 = 1u + (pt.m >> 31);  // 1 (pt.m < 2^31), opaque: see borrow_fma
 #pragma unroll
   for (int g0 = 0; g0 < CPL; g0 += G) {
     uint32_t qlen = 0;
@@ -509,8 +526,8 @@ __device__ __forceinline__ void filter_tile_q(const Pat& pt, const uint8_t* buf,
       const uint32_t c = cw0 + it * 32u + lane;
       SMGPU_DCHECK(pt.pre + 16u * c + 16u <= pt.lim);
       bool hit;
-      if constexpr (PA) hit = pair_hit<QA, WA>(buf, c, pt.pre, pt.s2, pt.bc1, pt.bc2);
-      else hit = chunk_hit(lds128(buf + pt.pre + 16u * c), pt.bc1);
+      if constexpr (PA) hit = pair_hit<QA, WA>(buf, c, pt.pre, pt.s2, pt.bc1, pt.bc2, k1);
+      else hit = chunk_hit(lds128(buf + pt.pre + 16u * c), pt.bc1, k1);
       const uint32_t bal = __ballot_sync(0xFFFFFFFFu, hit);
       if (hit) qc[qlen + __popc(bal & lanemask_lt())] = (uint16_t)c;
       qlen += __popc(bal);
@@ -559,26 +576,28 @@ __device__ __forceinline__ void pair_tile(const Pat& pt, const uint8_t* buf, uin
 
 // One BLOCK step (pattern offset off, broadcast symbol bc) over the CPL chunks of a lane.
 template <int CPL, int Q>
-__device__ __forceinline__ void block_step_q(Found4 (&F)[CPL], const uint8_t* cbase, uint32_t off, uint32_t bc) {
+__device__ __forceinline__ void block_step_q(Found4 (&F)[CPL], const uint8_t* cbase, uint32_t off, uint32_t bc,
+                                             uint32_t k1) {
   const uint32_t sh = (off & 3u) * 8u;
   const uint8_t* b = cbase + (off & ~15u);
 #pragma unroll
-  for (int it = 0; it < CPL; ++it) found_and_eq(F[it], window16_q<Q>(b + it * 512u, sh), bc);
+  for (int it = 0; it < CPL; ++it) found_and_eq(F[it], window16_q<Q>(b + it * 512u, sh), bc, k1);
 }
 
 template <int CPL>
 __device__ __forceinline__ void block_step(Found4 (&F)[CPL], const uint8_t* cbase, uint32_t e) {
   const uint32_t off = e & 0xFFFFu, bc = (e >> 16) * 0x01010101u;
+  const uint32_t k1 = 1u + (e >> 31);  // 1 (symbols < 256), opaque (eq_flags_fma)
   if ((off & 15u) == 0) {  // 16-B aligned window: one LDS.128, no shifts
 #pragma unroll
-    for (int it = 0; it < CPL; ++it) found_and_eq(F[it], lds128(cbase + off + it * 512u), bc);
+    for (int it = 0; it < CPL; ++it) found_and_eq(F[it], lds128(cbase + off + it * 512u), bc, k1);
     return;
   }
   switch ((off >> 2) & 3u) {  // warp-uniform
-    case 0: block_step_q<CPL, 0>(F, cbase, off, bc); break;
-    case 1: block_step_q<CPL, 1>(F, cbase, off, bc); break;
-    case 2: block_step_q<CPL, 2>(F, cbase, off, bc); break;
-    default: block_step_q<CPL, 3>(F, cbase, off, bc); break;
+    case 0: block_step_q<CPL, 0>(F, cbase, off, bc, k1); break;
+    case 1: block_step_q<CPL, 1>(F, cbase, off, bc, k1); break;
+    case 2: block_step_q<CPL, 2>(F, cbase, off, bc, k1); break;
+    default: block_step_q<CPL, 3>(F, cbase, off, bc, k1); break;
   }
 }
 

@@ -14,15 +14,22 @@ strat = int(sys.argv[5]) if len(sys.argv) > 5 else 0
 spec = synth.text_spec(cfg, n=n)
 t = synth.gen_text_device(spec, 0, n)
 h = sm.sm_histogram(t).cpu().numpy().astype(np.uint64)
-pats = [p.data for p in synth.patterns(cfg, spec=spec, lengths=[m], per_m=P) if p.kind == "sampled"][:P]
+pats = [p.data for p in synth.patterns(cfg, spec=spec, lengths=[m], per_m=max(P, 50)) if p.kind == "sampled"][:P]
 pb = sm.PatternBatch(pats)
 d = torch.zeros(pb.P, dtype=torch.int64, device="cuda")
 plans = {}
 for p in pats:
     s_, r_ = sm.sm_plan(p, h, strategy=strat)
     plans[(sm.STRATEGY_NAMES[s_], r_)] = plans.get((sm.STRATEGY_NAMES[s_], r_), 0) + 1
-for it in range(3):
+iters = int(os.environ.get("KCOUNT_ITERS", "3"))  # > 3: also the mean of the later half (sustained, power-capped)
+times = []
+for it in range(iters):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(); sm.sm_count_batch(pb, t, d, hist=h, strategy=strat); e1.record(); torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-print(f"{cfg} m={m} P={pb.P} n={n}: {ms:.3f} ms = {n * pb.P / ms / 1e6:.1f} GB/s per pattern; plans {plans}")
+    times.append(e0.elapsed_time(e1))
+ms = times[2] if iters >= 3 else times[-1]
+extra = ""
+if iters > 3:
+    late = times[iters // 2:]
+    extra = f"; sustained (iters {iters // 2}..{iters - 1}) {n * pb.P / (sum(late) / len(late)) / 1e6:.1f} GB/s"
+print(f"{cfg} m={m} P={pb.P} n={n}: {ms:.3f} ms = {n * pb.P / ms / 1e6:.1f} GB/s per pattern{extra}; plans {plans}")
