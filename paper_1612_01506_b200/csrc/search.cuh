@@ -22,8 +22,11 @@ constexpr int kBatchTableWords = kTableLarge;            // batching: table entr
 //                       [dispatched item per stage u32][PACKED code buffers][ring]   (the pattern tables stay in the kernel parameters)
 constexpr uint32_t kWarpTotOff = 2 * kMaxStages * 8;
 constexpr uint32_t kQueueOff = kWarpTotOff + 2 * kConsumerWarps * 4;
-constexpr uint32_t kTixOff = kQueueOff + kConsumerWarps * kQueueLen * 2;  // [kMaxStages] u32 dispatched items
-constexpr uint32_t kTblOff = kTixOff + kMaxStages * 4;                      // end of the fixed region
+// [kMaxStages] uint4 dispatched items {w, pattern k, tile ti, edge}: the producer maps w once
+// per item, the 8 consumer warps read the result with one LDS.128
+constexpr uint32_t kTixOff = kQueueOff + kConsumerWarps * kQueueLen * 2;
+static_assert(kTixOff % 16 == 0, "tix slots are read as uint4");
+constexpr uint32_t kTblOff = kTixOff + kMaxStages * 16;                     // end of the fixed region
 constexpr uint32_t kNoItem = 0xFFFFFFFFu;  // dispatched-item sentinel: the producer is done
 
 // kPackedB: b-bit codes; kPair: FILTER whose chunk test covers pi(1) and pi(2) together

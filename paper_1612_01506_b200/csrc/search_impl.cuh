@@ -200,7 +200,7 @@ struct WorkIter {
 // item in tix[stage] before arming the stage; consumers read it after the stage's wait.
 template <int EPI, int CAP, bool PRE = false, int CB = 1>
 __device__ void produce(const LaunchParams<CAP>& P, uint8_t* ring, uint64_t* full, uint64_t* empty,
-                        uint32_t* tix) {
+                        uint4* tix) {
   const LaunchArgs& a = P.a;
   const uint64_t pol = a.l2_policy == 2 ? l2_policy_evict_last()
                        : a.l2_policy == 1 ? l2_policy_evict_normal() : l2_policy_evict_first();
@@ -222,7 +222,8 @@ __device__ void produce(const LaunchParams<CAP>& P, uint8_t* ring, uint64_t* ful
     }
     const PatDesc& d = P.d[k];
     if (wrapped) mbar_wait_sleep(&empty[s], ph ^ 1u);  // consumers released this stage's previous use
-    if (dyn) tix[s] = (uint32_t)w;  // published by the arrive below (release)
+    if (dyn)  // published by the arrive below (release)
+      tix[s] = make_uint4((uint32_t)w, k, (uint32_t)ti, (ti < d.edge_lo || ti >= d.edge_hi) ? 1u : 0u);
     uint8_t* buf = ring + (size_t)s * a.stage_stride;
     if (PRE) {  // the tile's codes: one bulk copy from the padded code array (16-B granules)
       const uint64_t lo = ((d.k_begin + ti) * a.tile * CB) / 8u;
@@ -267,7 +268,7 @@ __device__ void produce(const LaunchParams<CAP>& P, uint8_t* ring, uint64_t* ful
   }
   if (dyn) {  // end of work: the next stage carries the sentinel (no bytes)
     if (wrapped) mbar_wait_sleep(&empty[s], ph ^ 1u);
-    tix[s] = kNoItem;
+    tix[s].x = kNoItem;
     mbar_arrive(&full[s]);
   }
 }
@@ -1080,7 +1081,7 @@ __global__ void __launch_bounds__(kThreads,
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + kMaxStages;
   uint32_t* s_wt = reinterpret_cast<uint32_t*>(smem + kWarpTotOff);  // [2][W]
-  uint32_t* tix = reinterpret_cast<uint32_t*>(smem + kTixOff);       // [stages] dispatched items
+  uint4* tix = reinterpret_cast<uint4*>(smem + kTixOff);             // [stages] dispatched items
   uint8_t* ring = smem + a.ring_off;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1120,13 +1121,16 @@ __global__ void __launch_bounds__(kThreads,
   const bool dyn = EPI != kEpiWrite && a.work_ctr != nullptr;
   uint32_t k;
   uint64_t ti;
+  bool pub_edge = false;
   while (true) {
     if (dyn) {  // the stage's item, published by the producer with the stage
       if (a.wait_ns) mbar_wait_sleep(&full[s], ph, a.wait_ns);
       else mbar_wait(&full[s], ph);
-      const uint32_t w = tix[s];
-      if (w == kNoItem) break;
-      items.map(P, w, k, ti);
+      const uint4 tw = tix[s];  // {w, k, ti, edge}, mapped by the producer
+      if (tw.x == kNoItem) break;
+      k = tw.y;
+      ti = tw.z;
+      pub_edge = tw.w != 0u;
     } else if (!items.advance(P, k, ti)) {
       break;
     }
@@ -1145,7 +1149,7 @@ __global__ void __launch_bounds__(kThreads,
     }
     const uint8_t* buf = ring + (size_t)s * a.stage_stride;
     const Pat pt{d.m, d.r, d.a1, d.bc1, d.s2, d.bc2, d.pre, (d.flags >> 8) & 0xFFu, d.stage_len, P.e + d.tbl};
-    const bool edge = ti < d.edge_lo || ti >= d.edge_hi;  // tile holds invalid alignments
+    const bool edge = dyn ? pub_edge : (ti < d.edge_lo || ti >= d.edge_hi);  // tile holds invalid alignments
     const int64_t shift = (STRAT == kFilter || STRAT == kPair) ? (int64_t)d.a1 : 0;
     const int64_t x_base = (int64_t)((d.k_begin + ti) * T) - shift;  // alignment offset of u = 0
     const int64_t pos_base = x_base - (int64_t)a.delta + (int64_t)a.pos_offset;  // position of u = 0
