@@ -3,8 +3,13 @@
 // and orders comparisons by "their probabilities in the text"; the
 // north star reads this as the histogram of t itself (reading R10).
 //
-// Persistent grid; 16-B streaming loads (L1 no-allocate, L2 evict-first); per-warp
-// privatised u32 bins in shared memory; one u64 atomic per (block, bin).
+// Persistent grid; 16-B streaming loads (ld.global.cs), 4 in flight per
+// thread; per-warp privatised u32 bins in shared memory (one ATOMS.POPC.INC per byte: lanes
+// incrementing the same bin are combined by the hardware); one u64 atomic per (block, bin).
+// Bound: shared-memory atomic throughput, not HBM -- random bytes spread a warp's 32
+// increments over random banks (~3.5-way conflicts): 2.6 TB/s on uniform bytes, 5.3 TB/s on
+// skewed or periodic text (tools/hist_probe.py: bin replicas per lane group and 4 or 16
+// warps per block were slower).  Once per text, amortised over every pattern pass.
 #include "device_util.cuh"
 #include "launch.h"
 
@@ -24,26 +29,30 @@ __global__ void __launch_bounds__(kHistWarps * 32) hist_kernel(const uint8_t* __
   const uint64_t head = ((16 - (ta & 15)) & 15) < n ? ((16 - (ta & 15)) & 15) : n;  // bytes before 16-B alignment
   const uint64_t nvec = (n - head) / 16;
   const uint4* v = reinterpret_cast<const uint4*>(t + head);
-  const uint64_t pol = l2_policy_evict_first();
 
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   SMGPU_DCHECK(head <= n && head + nvec * 16 <= n);
-  // 2 loads in flight per thread per iteration
-  for (; i + stride < nvec; i += 2 * stride) {
-    const uint4 a = ldg_v4_stream(v + i, pol);
-    const uint4 b = ldg_v4_stream(v + i + stride, pol);
-    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  // 4 loads in flight per thread per iteration (2: -7 to -10 %, tools/hist_probe.py; the
+  // L2::cache_hint evict-first form of the search kernel's loads: -10 % here)
+  for (; i + 3 * stride < nvec; i += 4 * stride) {
+    uint4 a[4];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      atomicAdd(&h[w[k] & 0xFF], 1u);
-      atomicAdd(&h[(w[k] >> 8) & 0xFF], 1u);
-      atomicAdd(&h[(w[k] >> 16) & 0xFF], 1u);
-      atomicAdd(&h[w[k] >> 24], 1u);
+    for (int u = 0; u < 4; ++u) a[u] = __ldcs(v + i + u * stride);  // ld.global.cs (evict-first)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t w[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        atomicAdd(&h[w[k] & 0xFF], 1u);
+        atomicAdd(&h[(w[k] >> 8) & 0xFF], 1u);
+        atomicAdd(&h[(w[k] >> 16) & 0xFF], 1u);
+        atomicAdd(&h[w[k] >> 24], 1u);
+      }
     }
   }
   for (; i < nvec; i += stride) {
-    const uint4 a = ldg_v4_stream(v + i, pol);
+    const uint4 a = __ldcs(v + i);
     const uint32_t w[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
