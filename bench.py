@@ -45,6 +45,7 @@ sys.path.insert(0, ROOT)
 
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0
+SPEC_HBM_GBS = 8000.0  # B200 HBM3e spec (north star: ">= 70 % of B200 HBM read bandwidth" = 5.6 TB/s)
 METRIC = "text GB/s scanned per pattern (device-timed) vs m; % of B200 HBM peak, 1/2/4/8 GPU"
 
 
@@ -263,12 +264,12 @@ def cpu_oracle_sample(spec, pats, seconds: float, threads: int):
             done += len(batch)
             i += threads
     dt = time.perf_counter() - t0
-    # single-thread oracle per pattern length: 2 patterns per m on an 8 MiB prefix
+    # single-thread oracle per pattern length: 3 patterns per m on an 8 MiB prefix
     small = text[: min(sample_n, 8 << 20)]
     per_m = {}
     for m in sorted(by_m):
         ts = time.perf_counter()
-        k = min(2, len(by_m[m]))
+        k = min(3, len(by_m[m]))
         for p in by_m[m][:k]:
             oracle.naive_count(p, small)
         per_m[str(m)] = round(small.size * k / (time.perf_counter() - ts) / 1e9, 3)
@@ -280,7 +281,7 @@ def cpu_oracle_sample(spec, pats, seconds: float, threads: int):
         "sample": f"plain Alg. 1 (oracle/oracle.c, gcc -O2) counting {done} patterns of the config's lengths "
                   f"over the first {sample_n >> 20} MiB of the {spec.name} text, {threads} threads, {dt:.1f} s",
         "single_thread_GBps_per_m": per_m,
-        "single_thread_sample": f"2 patterns per m over the first {small.size >> 20} MiB, one thread",
+        "single_thread_sample": f"3 patterns per m over the first {small.size >> 20} MiB, one thread",
     }
 
 
@@ -504,6 +505,7 @@ def run_native(args):
         ms = e0.elapsed_time(e1)
         gbs = float(local_bytes[idx].sum() / (ms * 1e-3) / 1e9)
         per_m[str(m)] = {"GBps": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4),
+                         "frac_of_spec_8TBps": round(gbs / SPEC_HBM_GBS, 4),
                          "us_per_launch": round(ms * 1e3 / len(idx), 2)}
     step()  # restore counts of the full step
     torch.cuda.synchronize()
@@ -700,6 +702,8 @@ def run_native(args):
             "kernel": "search_kernel (count)", "peak_kind": peak_kind,
             "algorithmic_bytes_per_launch": "n (text bytes of the launch's view)",
             "read_stream_probe": read_probe(),
+            # report all three denominators; the north star's ">= 70 %" is of the 8 TB/s spec
+            "spec_peak_GBps": SPEC_HBM_GBS, "frac_of_spec": round(achieved / SPEC_HBM_GBS, 4),
             "frac_of_read_stream_probe": (round(achieved / read_probe(), 4) if read_probe() else None),
             "frac_note": "achieved counts the algorithmic n bytes of every pattern pass; the DRAM traffic per pass is "
                          "`traffic` (< n: alternating passes of a batch reuse the 126 MB L2) and the peak is the "
