@@ -638,6 +638,12 @@ void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_
         uint32_t r1 = 0;
         while (r1 < d.r && (e[r1] & 0xFFFFu) < lim) ++r1;
         d.flags |= std::min<uint32_t>(r1, 255u) << 8;
+        // 1-bit codes, 32-alignment words (search_impl.cuh packed_tile, kWide): entry =
+        // offset | (1 - code) << 31, so a step gets its all-0 / all-1 mask word with ONE
+        // arithmetic shift (F &= window ^ mask) and uses the entry itself as the funnel-shift
+        // amount (mod 32)
+        if (cbits == 1 && L.cpl >= 2)
+          for (uint32_t j = 0; j < d.m; ++j) e[j] = (e[j] & 0xFFFFu) | ((((e[j] >> 16) & 1u) ^ 1u) << 31);
       }
     }
     L.a.stages = std::min<uint32_t>(stages, pre ? tunables().max_stages_pre : tunables().max_stages);

@@ -769,18 +769,21 @@ __device__ __forceinline__ int packed_tile(const Pat& pt, const uint8_t* buf, ui
       W0[it] = pk32[dc];
       W1[it] = pk32[dc + 1];
     }
+    // table entry e = off | (1 - code) << 31 (host, build_launch): the mask word
+    // nrep = ~(code broadcast) in one arithmetic shift, so a step is F &= window ^ nrep
+    // (one LOP3); the funnel shift takes e itself (amount mod 32)
     auto step_reg = [&](uint32_t e) {  // the window lies in W0:W1 (off < 32)
-      const uint32_t off = e & 0xFFFFu, rep = 0u - (e >> 16);
+      const uint32_t nrep = (uint32_t)((int32_t)e >> 31);
 #pragma unroll
-      for (int it = 0; it < D; ++it) F[it] &= ~(__funnelshift_r(W0[it], W1[it], off) ^ rep);
+      for (int it = 0; it < D; ++it) F[it] &= __funnelshift_r(W0[it], W1[it], e) ^ nrep;
     };
     auto step_mem = [&](uint32_t e) {  // off >= 32: two code words from shared memory
-      const uint32_t off = e & 0xFFFFu, rep = 0u - (e >> 16);
-      const uint32_t* p = pk32 + dc0 + (off >> 5);
+      const uint32_t nrep = (uint32_t)((int32_t)e >> 31);
+      const uint32_t* p = pk32 + dc0 + ((e & 0xFFFFu) >> 5);
 #pragma unroll
       for (int it = 0; it < D; ++it) {
         SMGPU_DCHECK((uint32_t)(p + it * 32 - pk32) + 1u < pk_words);
-        F[it] &= ~(__funnelshift_r(p[it * 32], p[it * 32 + 1], off & 31u) ^ rep);
+        F[it] &= __funnelshift_r(p[it * 32], p[it * 32 + 1], e) ^ nrep;
       }
     };
     auto step = [&](uint32_t e) {
