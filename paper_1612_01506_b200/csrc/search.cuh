@@ -15,6 +15,8 @@ constexpr uint32_t kLaneVerifyMaxM = 34;                 // FILTER: per-lane ver
 constexpr int kMaxBatch = 64;                            // patterns per launch
 constexpr int kListCap = 512;                            // reporting (overflow pass): buffered positions per warp and tile
 constexpr int kTableSmall = 256;                         // pattern-table capacities (u32 entries)
+constexpr int kTableMid = 2048;                          // (the launch cost grows with the parameter block:
+                                                         //  ~10 us at 8 KiB, ~27 us at 32 KiB on B200)
 constexpr int kTableLarge = 6400;                        // with 64 descriptors: fills the 32 KiB parameter space
 constexpr int kBatchTableWords = kTableLarge;            // batching: table entries per launch
 

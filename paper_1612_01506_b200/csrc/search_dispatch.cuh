@@ -53,6 +53,7 @@ cudaError_t launch_one(const HostLaunch& L, cudaStream_t st) {
 template <int STRAT, int EPI, int CPL>
 cudaError_t launch_cap(const HostLaunch& L, cudaStream_t st) {
   if (L.e.size() <= (size_t)kTableSmall) return launch_one<STRAT, EPI, kTableSmall, CPL>(L, st);
+  if (L.e.size() <= (size_t)kTableMid) return launch_one<STRAT, EPI, kTableMid, CPL>(L, st);
   return launch_one<STRAT, EPI, kTableLarge, CPL>(L, st);
 }
 
