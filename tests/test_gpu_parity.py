@@ -282,6 +282,40 @@ def test_count_batch_matches_oracle(sm):
                 assert got[i] == oracle.naive_count(p, view), (sigma, n, lim, i, len(p))
 
 
+@pytest.mark.parametrize("lengths", [
+    [8] * 32,                 # 256 table entries: the small parameter block
+    [8] * 32 + [1],           # 257: the 2048-entry block
+    [32] * 64,                # 2048
+    [32] * 63 + [33],         # 2049: the 6400-entry block
+    [100] * 64,               # 6400
+    [100] * 64 + [7],         # 6407: two launches
+])
+def test_batch_table_capacity_boundaries(sm, lengths):
+    """Launch parameter blocks come in three table capacities (256 / 2048 / 6400 entries,
+    search_dispatch.cuh launch_cap); batches whose tables sit on either side of each bound
+    must count and report exactly like the oracle (every strategy's launch path)."""
+    rng = np.random.default_rng(len(lengths) * 1000 + sum(lengths))
+    n = 200_003
+    a = rng.integers(0, 4, n, dtype=np.uint8) + 65  # 'A'..'D': dense enough to report
+    pats = []
+    for m in lengths:
+        s = int(rng.integers(0, n - m + 1))
+        pats.append(a[s:s + m].tobytes())
+    want = [oracle.naive_count(p, a) for p in pats]
+    t = dev(a, 5)
+    h = oracle.hist(a)
+    for strat in (1, 2, 3, 4):
+        d = torch.full((len(pats),), -1, dtype=torch.int64, device="cuda")
+        sm.sm_count_batch(pats, t, d, hist=h, strategy=strat)
+        assert d.cpu().tolist() == want, (strat, len(lengths))
+    d = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
+    pos = torch.empty(max(sum(want), 1), dtype=torch.int64, device="cuda")
+    sm.sm_report_batch(pats, t, pos, d)
+    assert d.cpu().tolist() == want
+    wp = np.concatenate([oracle.naive_report(p, a) for p in pats]) if sum(want) else np.zeros(0, np.uint64)
+    assert np.array_equal(pos[: sum(want)].cpu().numpy().astype(np.uint64), wp)
+
+
 def test_count_batch_strategies_agree(sm):
     spec = synth.text_spec("c2", n=(1 << 21) + 5)
     a = spec.host()
