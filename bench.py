@@ -122,10 +122,16 @@ def golden_check(config: str, counts, n: int, P: int):
             "count_sum": int(sum(want))}
 
 
-def traffic_per_pass(config: str):
+def traffic_per_pass(config: str, n: int):
+    """DRAM read+write bytes per pattern pass from the committed ncu capture of this config's
+    count kernel (profiles/traffic_<config>.json, tools/ncu_traffic.py), scaled to this run's n
+    when the capture ran on a prefix of the text (its traffic_over_algorithmic ratio)."""
     path = os.path.join(ROOT, "profiles", f"traffic_{config.lower()}.json")
     try:
-        return float(json.load(open(path))["traffic_per_pattern_pass"])
+        t = json.load(open(path))
+        if int(t["text_bytes"]) == int(n):
+            return float(t["traffic_per_pattern_pass"])
+        return float(t["traffic_over_algorithmic"]) * n
     except Exception:
         return None
 
@@ -697,7 +703,7 @@ def run_native(args):
             "frac": round(achieved / peak, 4),
             # DRAM read+write bytes per pattern pass, from the committed ncu --set full capture of
             # this kernel (profiles/traffic_c2.json, written by tools/ncu_traffic.py); null elsewhere
-            "traffic": traffic_per_pass(args.config),
+            "traffic": traffic_per_pass(args.config, spec.n),
             "traffic_unit": "bytes per pattern pass (algorithmic n = %d)" % spec.n, "avg_launch_us": round(search_ms * 1e3 / P, 2),
             "kernel": "search_kernel (count)", "peak_kind": peak_kind,
             "algorithmic_bytes_per_launch": "n (text bytes of the launch's view)",

@@ -69,6 +69,17 @@ def test_strong_and_weak_workloads(world):
     assert synth.text_spec("c5").n == 1 << 36
 
 
+def test_traffic_scales_a_prefix_capture_to_the_run():
+    import json
+    for cfg in ("c2", "c3", "c5"):
+        t = json.load(open(os.path.join(ROOT, "profiles", f"traffic_{cfg}.json")))
+        n = int(t["text_bytes"])
+        assert bench.traffic_per_pass(cfg, n) == t["traffic_per_pattern_pass"]
+        assert abs(bench.traffic_per_pass(cfg, 16 * n) - 16 * n * t["traffic_over_algorithmic"]) < 1.0
+        assert 0.5 < t["traffic_over_algorithmic"] < 1.1  # DRAM bytes per pass ~ n (less with L2 reuse)
+    assert bench.traffic_per_pass("c4", 1 << 32) is None  # compare-bound: no HBM traffic key
+
+
 def test_golden_check_catches_a_wrong_count():
     import json
     g = json.load(open(os.path.join(ROOT, "tests", "golden", "c1.json")))
