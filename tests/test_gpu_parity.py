@@ -316,6 +316,38 @@ def test_batch_table_capacity_boundaries(sm, lengths):
     assert np.array_equal(pos[: sum(want)].cpu().numpy().astype(np.uint64), wp)
 
 
+def test_count_batch_ordered_any_order_any_peel(sm):
+    """sm_count_batch_ordered (NEXT-2: the paper's fixed orders and r on the batched path):
+    every comparison order and peeling factor gives Alg. 1's count, for every
+    strategy, on binary / DNA / protein-like / wide alphabets."""
+    rng = np.random.default_rng(4242)
+    for sigma, n in ((2, 150_001), (4, 200_003), (20, 250_007), (96, 300_001)):
+        a = rng.integers(0, sigma, n, dtype=np.uint8) + (0x41 if sigma <= 96 else 0)
+        pats, orders, peels = [], [], []
+        for m in (1, 2, 3, 4, 7, 16, 33, 100):
+            for kind in range(4):
+                s = int(rng.integers(0, n - m + 1))
+                p = a[s:s + m].tobytes()
+                if kind == 0:
+                    o = list(range(m))                                  # Alg. 1 / 2 (identity)
+                elif kind == 1:
+                    o = sm.sm_heuristic_order(p, sm.SM_ORDER_PI_H)      # pi_h (PAPER.md:184)
+                elif kind == 2:
+                    o = sm.sm_heuristic_order(p, sm.SM_ORDER_PI_HS)     # pi_hs
+                else:
+                    o = rng.permutation(m).tolist()                     # any permutation
+                pats.append(p)
+                orders.append(o)
+                peels.append(int(rng.integers(0, m + 1)))               # 0 = auto, else 1..m
+        want = [oracle.naive_count(p, a) for p in pats]
+        t = dev(a, 7)
+        h = oracle.hist(a)
+        for strat in (0, 1, 2, 3, 4) if sigma <= 4 else (0, 1, 2, 4):  # forced PACKED needs <= 4 symbols
+            d = torch.full((len(pats),), -1, dtype=torch.int64, device="cuda")
+            sm.sm_count_batch_ordered(pats, t, d, orders=orders, peels=peels, hist=h, strategy=strat)
+            assert d.cpu().tolist() == want, (sigma, strat)
+
+
 def test_count_batch_strategies_agree(sm):
     spec = synth.text_spec("c2", n=(1 << 21) + 5)
     a = spec.host()
