@@ -184,6 +184,23 @@ def test_report_truncation(sm):
     assert lib.sm_last_error() == sm.SM_ETRUNC
 
 
+@pytest.mark.parametrize("cap", [(1 << 20) + 17, 512 * 3000 + 34, 10])
+def test_report_truncated_dense_1gib(sm, cap):
+    """A truncated report of an everywhere-matching pattern on a 1 GiB text: the staged records
+    overflow the default staging pool (its last chunk partial, cap % 512 in 1..34 or tiny), so the
+    overflow pass and the chunk terminators are exercised.  Expected values are
+    the closed form of a^n / a^m (every alignment matches; pinned in tests/test_oracle.py)."""
+    n, m = 1 << 30, 17
+    t = torch.full((n,), 0x61, dtype=torch.uint8, device="cuda")
+    d = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    pos = torch.full((cap,), -7, dtype=torch.int64, device="cuda")
+    sm.sm_report_async(b"a" * m, t, pos, d)
+    assert int(d.item()) == n - m + 1
+    assert torch.equal(pos, torch.arange(cap, dtype=torch.int64, device="cuda"))
+    del t, pos
+    torch.cuda.empty_cache()
+
+
 def test_dense_report_every_alignment(sm):
     n = 300_003
     t = dev(np.full(n, 7, dtype=np.uint8), 3)
