@@ -86,6 +86,24 @@ def test_edge_cases(sm):
     assert sm.sm_count(b"\x00", dev(np.zeros(33, dtype=np.uint8))) == 33   # NUL is a symbol
 
 
+def test_maximum_pattern_length(sm):
+    """m = SM_MAX_PATTERN (4096): the longest halo and table; every strategy, count and report."""
+    M = sm.SM_MAX_PATTERN
+    rng = np.random.default_rng(M)
+    for sigma in (2, 4, 256):
+        a = (rng.integers(0, sigma, (1 << 20) + 3, dtype=np.uint8) + (0x41 if sigma <= 4 else 0)).astype(np.uint8)
+        a[200_000:200_000 + 3 * M] = np.tile(a[200_000:200_000 + M], 3)  # overlapping repeats -> several matches
+        p = a[200_000:200_000 + M].tobytes()
+        want = oracle.naive_count(p, a)
+        assert want >= 3
+        t = dev(a, 11)
+        h = oracle.hist(a)
+        for strat in ((0, 1, 2, 3, 4) if sigma <= 4 else (0, 1, 2, 4)):
+            assert count_async(sm, p, t, hist=h, strategy=strat) == want, (sigma, strat)
+        pos, total = sm.sm_report(p, t)
+        assert total == want and pos.cpu().numpy().astype(np.uint64).tolist() == oracle.naive_report(p, a).tolist()
+
+
 def test_errors(sm):
     t = dev(np.frombuffer(b"hello", dtype=np.uint8))
     with pytest.raises(sm.SmError) as e:
