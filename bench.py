@@ -70,6 +70,7 @@ def parse():
     return ap.parse_args()
 
 
+L2_FLUSH_BYTES = 256 << 20  # > 2x the 126 MB L2
 STRONG = {"c5"}  # configs whose total text is fixed as N grows (BASELINE.json configs[4])
 
 
@@ -200,6 +201,12 @@ class ClockSampler:
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         lines = [ln for t, ln in self.lines if (t0 is None or t >= t0) and (t1 is None or t <= t1 + 0.06)]
+        window = "timed region"
+        if not lines and t0 is not None and t1 is not None:
+            # a timed region shorter than the 50 ms sampling period (c1: ~2 ms): the samples
+            # nearest to it, taken while the warm GPU idles between the barriers
+            lines = [ln for t, ln in self.lines if t0 - 0.3 <= t <= t1 + 0.3]
+            window = f"+-0.3 s around a {1e3 * (t1 - t0):.1f} ms timed region"
         for ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 7:
@@ -214,7 +221,8 @@ class ClockSampler:
                     reasons.add(nm)
         sm.sort()
         med = sm[len(sm) // 2] if sm else None
-        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "window": window}
 
 
 # ----------------------------------------------------------------------------- workload
@@ -467,18 +475,34 @@ def run_native(args):
     launches0 = sm.sm_launch_count()
     evs = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # A shard that fits in the 126 MB L2 (c1: 1 MiB) would otherwise be served from L2 by every
+    # step after the first: write a buffer larger than L2 between timed steps and time each step
+    # on its own events (the flush stays outside them).  Larger shards stream from HBM anyway.
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev) \
+        if shard.held_len < L2_FLUSH_BYTES else None
+    step_ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(2)) for _ in range(args.steps)]
     barrier()
     h0 = clk.mark()
     start.record(stream)
     for s in range(args.steps):
+        if flush is not None:
+            flush.fill_(s)
+            step_ev[s][0].record(stream)
         step(evs[s])
+        if flush is not None:
+            step_ev[s][1].record(stream)
     end.record(stream)
     barrier()
     h1 = clk.mark()
     launches = sm.sm_launch_count() - launches0
     total_ms = start.elapsed_time(end)
+    if flush is not None:
+        total_ms = sum(a.elapsed_time(b) for a, b in step_ev)
+        del flush
     search_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps   # the P search launches of a step
     coll_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps     # the count all_reduce (N > 1)
+    if h1 - h0 < 0.2:
+        time.sleep(0.3)  # short region: let the sampler deliver the samples after it (stop()'s fallback window)
     clocks = clk.stop(h0, h1)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -685,7 +709,10 @@ def run_native(args):
         "config": {
             "workload": spec.name, "text_bytes": spec.n, "text_bytes_per_gpu": shard.owned_bytes,
             "patterns": P, "lengths": lens, "parallelism": f"text-shard x{world}",
-            "l2": "inputs larger than L2 (256 MiB/GPU vs 126 MB); TMA loads use L2 evict_first",
+            "l2": (f"inputs larger than L2 ({shard.held_len / 2**20:.0f} MiB/GPU vs 126 MB); "
+                   "TMA loads use L2 evict_first") if shard.held_len >= L2_FLUSH_BYTES else
+                  (f"text ({shard.held_len / 2**20:.0f} MiB) fits in L2: a {L2_FLUSH_BYTES >> 20} MiB buffer "
+                   "is written between timed steps, each step timed on its own events (flush excluded)"),
             "step": "hist + per-pattern order + batched count launches (each pattern a full pass) (+ all_reduce)",
             "halo_bytes": shard.halo,
         },
