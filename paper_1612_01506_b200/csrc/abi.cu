@@ -100,39 +100,44 @@ sm_status check_pattern_text(const uint8_t* p, size_t m, const uint8_t* t, size_
 
 // stable rarest-first order (ties by position, R11).  A stable
 // counting sort: the distinct key values hist[c] of the symbols in p are ranked
-// (at most 256 of them), then positions are bucketed by rank in ascending order.
-// O(m + 256 log 256); equals std::stable_sort by hist[p[j]].
+// (at most 256 of them), then positions are bucketed by rank in ascending order
+// (stable: ascending position within a bucket).  O(m + sigma_p^2) for sigma_p distinct
+// symbols in p; equals std::stable_sort by hist[p[j]].
 void order_from_hist(const uint64_t* hist, const uint8_t* p, size_t m, uint32_t* order) {
-  if (m <= 48) {  // short patterns: stable insertion sort of the positions by count
-    for (size_t j = 0; j < m; ++j) {
-      const uint64_t key = hist[p[j]];
-      size_t i = j;
-      while (i > 0 && hist[p[order[i - 1]]] > key) {
-        order[i] = order[i - 1];
-        --i;
-      }
-      order[i] = (uint32_t)j;
-    }
-    return;
-  }
-  bool present[256] = {false};
-  for (size_t j = 0; j < m; ++j) present[p[j]] = true;
+  // distinct symbols of p in first-occurrence order (a pattern holds few: 4 for DNA)
+  uint8_t slot[256];
+  uint64_t seen[4] = {0, 0, 0, 0};
   uint8_t syms[256];
   int ns = 0;
-  for (int c = 0; c < 256; ++c)
-    if (present[c]) syms[ns++] = (uint8_t)c;
-  std::sort(syms, syms + ns, [&](uint8_t x, uint8_t y) { return hist[x] < hist[y]; });
-  uint32_t rank[256];
+  for (size_t j = 0; j < m; ++j) {
+    const uint8_t c = p[j];
+    if (!(seen[c >> 6] >> (c & 63) & 1u)) {
+      seen[c >> 6] |= 1ull << (c & 63);
+      syms[ns++] = c;
+    }
+  }
+  // rank the distinct count values: insertion sort of the symbols by hist (ns is small)
+  for (int i = 1; i < ns; ++i) {
+    const uint8_t c = syms[i];
+    const uint64_t key = hist[c];
+    int k = i;
+    while (k > 0 && hist[syms[k - 1]] > key) {
+      syms[k] = syms[k - 1];
+      --k;
+    }
+    syms[k] = c;
+  }
+  uint32_t start[257];
   int nr = 0;
   for (int i = 0; i < ns; ++i) {
     if (i > 0 && hist[syms[i]] != hist[syms[i - 1]]) ++nr;
-    rank[syms[i]] = (uint32_t)nr;
+    slot[syms[i]] = (uint8_t)nr;
   }
   ++nr;
-  uint32_t start[257] = {0};
-  for (size_t j = 0; j < m; ++j) ++start[rank[p[j]] + 1];
+  for (int r = 0; r <= nr; ++r) start[r] = 0;
+  for (size_t j = 0; j < m; ++j) ++start[slot[p[j]] + 1];
   for (int r = 0; r < nr; ++r) start[r + 1] += start[r];
-  for (size_t j = 0; j < m; ++j) order[start[rank[p[j]]]++] = (uint32_t)j;
+  for (size_t j = 0; j < m; ++j) order[start[slot[p[j]]]++] = (uint32_t)j;
 }
 
 bool valid_permutation(const uint32_t* order, size_t m) {
@@ -421,7 +426,8 @@ sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist
     // has a flat cost and wins only when even the pair test passes most chunks (m >= 3).
     // Crossovers measured on B200 (tools/pair_sweep.sh, profiles/strategy_r1.md).
     const double f1 = freq(0), f12 = m >= 2 ? f1 * freq(1) : f1;
-    const double h1 = 1.0 - std::pow(1.0 - f1, 16.0), h12 = 1.0 - std::pow(1.0 - f12, 16.0);
+    auto pow16 = [](double x) { x *= x; x *= x; x *= x; return x * x; };
+    const double h1 = 1.0 - pow16(1.0 - f1), h12 = 1.0 - pow16(1.0 - f12);
     if (h12 > tunables().block_min_hit) {
       // m = 2: PAIR's pair test, taken per byte, is the match itself (one pass, no queue,
       // no phase B: search_impl.cuh filter_tile_q), so it replaces BLOCK at any density
