@@ -216,13 +216,34 @@ bool use_dispatch(uint64_t n, size_t P) {
   return tu.dispatch && n * P >= (P == 1 ? tu.dispatch_min_bytes_single : tu.dispatch_min_bytes);
 }
 
+// The comparison order of one plan: inline for m <= 64 (no allocation per pattern on
+// the planning path of a batch call), on the heap beyond.
+class OrderVec {
+ public:
+  void resize(size_t m) {
+    m_ = m;
+    if (m > kInline) heap_.resize(m);
+  }
+  size_t size() const { return m_; }
+  uint32_t* data() { return m_ > kInline ? heap_.data() : small_; }
+  const uint32_t* data() const { return m_ > kInline ? heap_.data() : small_; }
+  uint32_t& operator[](size_t k) { return data()[k]; }
+  const uint32_t& operator[](size_t k) const { return data()[k]; }
+
+ private:
+  static constexpr size_t kInline = 64;
+  size_t m_ = 0;
+  uint32_t small_[kInline];
+  std::vector<uint32_t> heap_;
+};
+
 struct Plan {
   int strategy = kFilter;
   uint32_t code_shift = 0;  // PACKED: code field shift
   uint32_t r = 1;
   int cpl = 4;
   uint32_t tile = 16384;
-  std::vector<uint32_t> order;
+  OrderVec order;
 };
 
 
@@ -487,16 +508,28 @@ sm_status make_plan(const uint8_t* p, size_t m, uint64_t n, const uint64_t* hist
 }
 
 sm_status host_hist(const uint8_t* t, size_t n, cudaStream_t st, uint64_t* out) {
+  // the 2 KiB read-back lands in a pinned per-thread buffer (a pageable destination costs
+  // a staged, synchronous copy on the step's critical path: the host plans only after it)
+  static thread_local uint64_t* pinned = nullptr;
+  if (!pinned) {
+    void* hp = nullptr;
+    if (cudaHostAlloc(&hp, 256 * sizeof(uint64_t), cudaHostAllocPortable) == cudaSuccess)
+      pinned = static_cast<uint64_t*>(hp);
+    else
+      cudaGetLastError();  // clear it: fall back to the caller's (pageable) buffer
+  }
+  uint64_t* dst = pinned ? pinned : out;
   uint64_t* d = nullptr;
   SM_CUDA_TRY(pool_alloc(reinterpret_cast<void**>(&d), 256 * sizeof(uint64_t), st), "pool_alloc(hist)");
   cudaError_t e = launch_hist(t, n, d, num_sms(), st);
   if (e == cudaSuccess) {
     ++g_launches;
-    e = cudaMemcpyAsync(out, d, 256 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
+    e = cudaMemcpyAsync(dst, d, 256 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
   }
   cudaFreeAsync(d, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "histogram");
+  if (dst != out) std::memcpy(out, dst, 256 * sizeof(uint64_t));
   return SM_OK;
 }
 
@@ -573,6 +606,9 @@ void build_launch(const std::vector<const Planned*>& ps, const uint8_t* t, size_
   const bool pre = is_prepacked(L.strategy);
   const uint32_t cbits = (uint32_t)code_bits(L.strategy);
   L.a.code_shift = ps[0]->pl.code_shift;
+  size_t words = 0;
+  for (const Planned* q : ps) words += q->m;
+  L.e.reserve(words);
   for (const Planned* q : ps) {
     for (size_t k = 0; k < q->m; ++k) {
       const uint32_t sym = q->p[q->pl.order[k]];
