@@ -111,3 +111,32 @@ def test_reference_arm_under_torchrun_two_ranks():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["config"]["world"] == 2
     assert d["cpu_baseline"]["kind"] == "oracle" and d["value"] > 0
+
+
+def test_clock_sampler_short_region_window():
+    """A timed region shorter than the 50 ms sampling period takes the samples within
+    +-0.3 s of it (and says so); a long region keeps only its own samples."""
+    c = bench.ClockSampler(0)
+
+    class _P:
+        def terminate(self):
+            pass
+
+        def wait(self, timeout=None):
+            return 0
+
+    c.proc = _P()
+    row = "1965, 1965, 700.0, Not Active, Not Active, Not Active, {}"
+    c.lines = [(10.00, row.format("Not Active")), (10.25, row.format("Active")), (11.0, row.format("Not Active"))]
+    short = c.stop(10.1, 10.102)
+    assert short["samples"] == 2 and short["reasons"] == ["sw_power_cap"] and "around" in short["window"]
+    c.proc = _P()
+    long_ = c.stop(10.2, 10.9)
+    assert long_["samples"] == 1 and long_["window"] == "timed region" and long_["sm_mhz"] == 1965.0
+
+
+def test_l2_flush_threshold():
+    """Shards below the flush size (c1's 1 MiB) get an L2 flush between timed steps;
+    the default c2 shard (256 MiB + halo) streams from HBM without one."""
+    assert bench.L2_FLUSH_BYTES >= 2 * 126 * 10**6
+    assert (1 << 20) < bench.L2_FLUSH_BYTES <= (256 << 20) + 1023
