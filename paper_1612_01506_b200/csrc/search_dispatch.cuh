@@ -26,20 +26,32 @@ cudaError_t launch_one(const HostLaunch& L, cudaStream_t st) {
   // would run the round-robin work items after the first, a tail of up to 50 %
   int grid = L.grid;
   {
-    static thread_local size_t cached_smem = ~(size_t)0;
-    static thread_local int cached_dev = -1;
-    static thread_local int cached_blocks = 0;
-    if (cached_smem != L.smem || cached_dev != dev) {
-      int nb = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kfn, kThreads, L.smem) != cudaSuccess) nb = 0;
-      cached_smem = L.smem;
-      cached_dev = dev;
-      cached_blocks = nb;
+    // occupancy per (device, dynamic smem): the launches of one batch call differ in their
+    // stage size, so a few entries (round-robin replacement) keep the occupancy query, a
+    // few microseconds of host time, off every launch
+    struct OccEntry {
+      size_t smem;
+      int dev, blocks, sms;
+    };
+    constexpr int kOccEntries = 8;
+    static thread_local OccEntry occ[kOccEntries] = {};
+    static thread_local int occ_used = 0, occ_next = 0;
+    int hit = -1;
+    for (int i = 0; i < occ_used; ++i)
+      if (occ[i].smem == L.smem && occ[i].dev == dev) {
+        hit = i;
+        break;
+      }
+    if (hit < 0) {
+      OccEntry x{L.smem, dev, 0, 0};
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x.blocks, kfn, kThreads, L.smem) != cudaSuccess) x.blocks = 0;
+      if (cudaDeviceGetAttribute(&x.sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) x.sms = 0;
+      cudaGetLastError();  // a failed query only leaves the grid as planned
+      hit = occ_used < kOccEntries ? occ_used++ : occ_next++ % kOccEntries;
+      occ[hit] = x;
     }
-    int sms = 0;
-    if (cached_blocks > 0 &&
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0)
-      grid = grid < cached_blocks * sms ? grid : cached_blocks * sms;
+    const OccEntry& o = occ[hit];
+    if (o.blocks > 0 && o.sms > 0) grid = grid < o.blocks * o.sms ? grid : o.blocks * o.sms;
   }
   static thread_local LaunchParams<CAP> P;  // ~19 KiB for CAP = 4096: keep it off the stack
   P.a = L.a;
