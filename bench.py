@@ -732,6 +732,8 @@ def run_native(args):
             # this kernel (profiles/traffic_c2.json, written by tools/ncu_traffic.py); null elsewhere
             "traffic": traffic_per_pass(args.config, spec.n),
             "traffic_unit": "bytes per pattern pass (algorithmic n = %d)" % spec.n, "avg_launch_us": round(search_ms * 1e3 / P, 2),
+            # the same pass seen from DRAM: captured traffic per pass / this run's average pass time
+            **dram_side(traffic_per_pass(args.config, spec.n), search_ms * 1e-3 / P, peak),
             "kernel": "search_kernel (count)", "peak_kind": peak_kind,
             "algorithmic_bytes_per_launch": "n (text bytes of the launch's view)",
             "read_stream_probe": read_probe(),
@@ -740,7 +742,8 @@ def run_native(args):
             "frac_of_read_stream_probe": (round(achieved / read_probe(), 4) if read_probe() else None),
             "frac_note": "achieved counts the algorithmic n bytes of every pattern pass; the DRAM traffic per pass is "
                          "`traffic` (< n: alternating passes of a batch reuse the 126 MB L2) and the peak is the "
-                         "measured COPY (read+write) rate, so frac can exceed 1 for a read-only stream",
+                         "measured COPY (read+write) rate, so frac can exceed 1 for a read-only stream; "
+                         "dram_achieved / dram_frac are the same pass counted in DRAM bytes (traffic / avg_launch_us)",
         },
         "per_m": per_m,
         "clocks": clocks,
@@ -753,6 +756,16 @@ def run_native(args):
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def dram_side(traffic, pass_s, peak):
+    """DRAM-side rate of one pattern pass: ncu-captured DRAM bytes per pass / the live average pass time.
+
+    `frac` (algorithmic bytes) can exceed 1 when passes reuse the L2; `dram_frac` cannot."""
+    if not traffic or not pass_s or not peak:
+        return {"dram_achieved": None, "dram_frac": None}
+    gbs = traffic / pass_s / 1e9
+    return {"dram_achieved": round(gbs, 1), "dram_frac": round(gbs / peak, 4)}
 
 
 def main():

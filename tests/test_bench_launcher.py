@@ -140,3 +140,13 @@ def test_l2_flush_threshold():
     the default c2 shard (256 MiB + halo) streams from HBM without one."""
     assert bench.L2_FLUSH_BYTES >= 2 * 126 * 10**6
     assert (1 << 20) < bench.L2_FLUSH_BYTES <= (256 << 20) + 1023
+
+
+def test_dram_side_of_the_roofline():
+    """roofline.dram_frac = captured DRAM bytes per pass / live pass time / peak; null without a capture."""
+    import bench
+    d = bench.dram_side(195931006.5, 34.01e-6, 6461.5)
+    assert abs(d["dram_achieved"] - 5761.0) < 1.0 and abs(d["dram_frac"] - 0.8916) < 2e-4
+    assert d["dram_frac"] < 1.0
+    assert bench.dram_side(None, 34.01e-6, 6461.5) == {"dram_achieved": None, "dram_frac": None}
+    assert bench.dram_side(1.0, 0.0, 6461.5) == {"dram_achieved": None, "dram_frac": None}
