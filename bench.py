@@ -761,7 +761,9 @@ def run_native(args):
 def dram_side(traffic, pass_s, peak):
     """DRAM-side rate of one pattern pass: ncu-captured DRAM bytes per pass / the live average pass time.
 
-    `frac` (algorithmic bytes) can exceed 1 when passes reuse the L2; `dram_frac` cannot."""
+    `frac` (algorithmic bytes) exceeds 1 when passes reuse the L2; `dram_frac` counts only what DRAM
+    moved (it still passes 1 by a few percent where a read-only stream outruns the read+write copy
+    the peak was measured with: c5, 7.56 TB/s probe vs the 6.46 TB/s copy)."""
     if not traffic or not pass_s or not peak:
         return {"dram_achieved": None, "dram_frac": None}
     gbs = traffic / pass_s / 1e9
