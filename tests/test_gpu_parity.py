@@ -549,6 +549,65 @@ def test_concurrent_streams(sm):
         assert d.cpu().tolist() == [oracle.naive_count(p, a) for p in pats]
 
 
+def test_concurrent_host_threads(sm):
+    """Re-entrancy across HOST threads (smgpu.h "Concurrency"): four threads call the library at
+    the same time (ctypes releases the GIL inside each call), each on its own stream with its own
+    text -- count batches that histogram the text themselves (per-thread pinned read-back,
+    per-thread launch tables and occupancy cache, the shared scratch pool), reports through the
+    pool's staging buffers, and the synchronous sm_count on cudaStreamPerThread.  Every result
+    equals the oracle's, and the thread-local status of one thread's failing call (m = 0) does
+    not leak into another's."""
+    import threading
+
+    rng = np.random.default_rng(81)
+    sigmas = (2, 4, 20, 256)
+    texts = [rng.integers(0, s, 700_001 + 13 * i, dtype=np.uint8) for i, s in enumerate(sigmas)]
+    devs = [dev(a, i) for i, a in enumerate(texts)]
+    plan = []
+    for a in texts:
+        pats = [a[s:s + m].tobytes() for m in (1, 2, 3, 7, 16, 40, 257) for s in rng.integers(0, a.size - m, 3)]
+        plan.append((pats, [oracle.naive_count(p, a) for p in pats],
+                     oracle.naive_report(pats[9], a).astype(np.int64)))
+    torch.cuda.synchronize()
+    errors = []
+    start = threading.Barrier(len(texts))
+
+    def work(k):
+        try:
+            torch.cuda.set_device(0)
+            a, t = texts[k], devs[k]
+            pats, want, want_pos = plan[k]
+            st = torch.cuda.Stream()
+            start.wait()
+            for it in range(6):
+                with torch.cuda.stream(st):
+                    d = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
+                    sm.sm_count_batch(pats, t, d, stream=st)           # library histogram inside
+                    pos, total = sm.sm_report(pats[9], t)               # cudaStreamPerThread, synchronous
+                    got1 = sm.sm_count(pats[(it * 5) % len(pats)], t)
+                    if k == it % len(texts):
+                        with pytest.raises(Exception):
+                            sm.sm_count(b"", t)                         # SM_EINVAL on this thread only
+                st.synchronize()
+                assert d.cpu().tolist() == want, (k, it)
+                assert total == want_pos.size and np.array_equal(pos.cpu().numpy(), want_pos), (k, it)
+                assert got1 == want[(it * 5) % len(pats)], (k, it)
+        except BaseException as e:  # noqa: BLE001 -- reported by the main thread
+            errors.append((k, repr(e)))
+            try:
+                start.abort()
+            except Exception:
+                pass
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(len(texts))]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join(timeout=300)
+    assert not any(th.is_alive() for th in threads), "a worker thread hung"
+    assert not errors, errors
+
+
 def test_report_sharded_virtual(sm):
     """NEXT-4: per-shard reports with global positions (position_offset), concatenated per
     pattern in rank order == the 1-GPU report."""
